@@ -1,0 +1,207 @@
+/*
+ * runlora.h — C ABI of the B200 (sm_100a) RunLoRA hot path.
+ *
+ * The operation (arXiv 2312.03415, PAPER.md):
+ *   forward   Y  = X W + (X A) B          (forward1, Eq. 1)
+ *             Y  = X (W + A B)            (forward2, Eq. 2)
+ *   backward  dA = Xᵀ dY Bᵀ,  dB = Aᵀ Xᵀ dY,  dX = dY Wᵀ + dY Bᵀ Aᵀ   (Eq. 3)
+ *             evaluated by one of the bracketings backward1..backward5
+ *             (Algorithms 1-5); backward6..8 exist for
+ *             cost queries only.
+ *   cost      Table 1, exact integers; Eq. 5 parameter-reduction
+ *             predicate r(i+o) < io.
+ *   select    "best forward and backward computation graph based on FLOPs and
+ *             time estimations" (abstract, P:5).
+ * Nothing from X·A is saved between forward and backward: every backward
+ * entry point takes only X, W, A, B, dY.
+ *
+ * Notation: n = b·s tokens, k = input dim (paper i), m = output dim (paper o),
+ * r = rank.  All matrices are ROW-MAJOR, contiguous, in the paper's orientation:
+ *   X[n,k]  W[k,m]  A[k,r]  B[r,m]  Y,dY[n,m]  dX[n,k]  dA[k,r]  dB[r,m]
+ *
+ * Pointers:
+ *   - Every matrix pointer passed to forward/backward/select is a DEVICE pointer
+ *     (cudaMalloc / caching allocator memory of the handle's device) unless the
+ *     parameter name ends in _host (pinned or pageable host memory).
+ *   - Device pointers must be 16-byte aligned.
+ *   - The caller owns every buffer, including the workspace; the library never
+ *     allocates device memory on the forward/backward path.  The handle owns only
+ *     host-side caches (TMA descriptors, plans, profiling events).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     All calls are asynchronous and stream-ordered; argument validation is
+ *     synchronous and happens before anything is launched.
+ *
+ * Dtypes: RUNLORA_F32 computes every product in true fp32 FFMA (no TF32);
+ * RUNLORA_BF16 reads bf16 operands, accumulates in fp32 on the tcgen05 tensor
+ * cores and stores Y, dX and the rank-r intermediates in bf16; W+AB is formed in
+ * fp32 and rounded once (R10).  For bf16, k, m and r must be multiples
+ * of 8 (TMA needs 16-byte row strides) — otherwise RUNLORA_ERR_ALIGNMENT.
+ *
+ * Errors: a non-zero runlora_status_t; runlora_last_error() returns a
+ * thread-local message naming the offending argument(s).  No C++ exception
+ * crosses this boundary.  Asynchronous device faults surface at the caller's
+ * next synchronisation.
+ */
+#ifndef RUNLORA_H_
+#define RUNLORA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RUNLORA_ABI_VERSION 1
+
+typedef enum {
+  RUNLORA_OK = 0,
+  RUNLORA_ERR_INVALID_ARG = 1,      /* null pointer, n/k/m/r <= 0, bad enum */
+  RUNLORA_ERR_SHAPE = 2,            /* inconsistent shapes */
+  RUNLORA_ERR_DTYPE = 3,            /* unsupported dtype combination */
+  RUNLORA_ERR_UNSUPPORTED_VARIANT = 4, /* backward6..8 passed to an execute call */
+  RUNLORA_ERR_OVERFLOW = 5,         /* FLOP count does not fit in uint64 */
+  RUNLORA_ERR_ALIGNMENT = 6,        /* pointer not 16B aligned, or bf16 k/m/r not multiple of 8 */
+  RUNLORA_ERR_WORKSPACE = 7,        /* workspace smaller than runlora_workspace_size() */
+  RUNLORA_ERR_CUDA = 8,             /* a CUDA runtime/driver call or launch failed */
+  RUNLORA_ERR_TIMING = 9,           /* time-based selection could not measure */
+  RUNLORA_ERR_DEVICE = 10           /* device is not sm_100 (B200) */
+} runlora_status_t;
+
+typedef enum { RUNLORA_F32 = 0, RUNLORA_BF16 = 1 } runlora_dtype_t;
+
+/* Forward variant numbers: 1 = forward1 (Eq. 1), 2 = forward2 (Eq. 2).
+ * Backward variant numbers: 1..8 = backwardN; 1..5 executable. */
+typedef enum { RUNLORA_BY_FLOPS = 0, RUNLORA_BY_TIME = 1, RUNLORA_HYBRID = 2 } runlora_criterion_t;
+
+typedef struct {
+  int64_t n, k, m, r;   /* tokens (b·s), in (i), out (o), rank */
+  int32_t dtype;        /* runlora_dtype_t of X, W, A, B, dY, Y, dX */
+} runlora_shape_t;
+
+typedef struct {
+  int32_t fwd;                 /* chosen forward variant (1|2) */
+  int32_t bwd;                 /* chosen backward variant (1..5) */
+  int32_t criterion;           /* runlora_criterion_t used */
+  int32_t param_reduction;     /* Eq. 5 holds (1) or not (0); a violation is not an error */
+  uint64_t flops_fwd[3];       /* index = variant number; [0] unused */
+  uint64_t flops_bwd[9];       /* index = variant number 1..8; [0] unused */
+  float time_fwd_us[3];        /* median device time per candidate; NaN if not timed */
+  float time_bwd_us[9];
+  int32_t flops_fwd_pick;      /* the FLOP-criterion pick, always reported */
+  int32_t flops_bwd_pick;
+} runlora_plan_t;
+
+/* Device operand set for time-based selection (all device pointers, caller-owned;
+ * Y, dX, dA, dB are overwritten while candidates are timed). */
+typedef struct {
+  const void *X, *W, *A, *B, *dY;
+  void *Y, *dX, *dA, *dB;
+  int32_t grad_dtype;          /* runlora_dtype_t of dA/dB */
+} runlora_operands_t;
+
+typedef struct runlora_handle_s* runlora_handle_t;
+
+/* Per-kernel profile record (runlora_profile_read). */
+typedef struct {
+  char name[48];
+  uint64_t launches;
+  double total_ms;   /* sum of CUDA-event durations of this kernel's launches */
+} runlora_kernel_stat_t;
+
+/* ---------------------------------------------------------------- lifetime */
+const char* runlora_version(void);
+/* Creates a handle bound to CUDA `device`; fails with RUNLORA_ERR_DEVICE unless
+ * the device is compute capability 10.0 (sm_100a code only). */
+runlora_status_t runlora_create(runlora_handle_t* out, int device);
+runlora_status_t runlora_destroy(runlora_handle_t h);
+
+/* -------------------------------------------------------------- cost model
+ * Table 1 as printed, exact uint64 arithmetic (overflow-checked).
+ * is_backward = 0: variant in {1,2}; is_backward = 1: variant in {1..8}.
+ * dtype is ignored. */
+runlora_status_t runlora_flops(const runlora_shape_t* s, int is_backward, int variant, uint64_t* out);
+/* Eq. 5: 1 iff r(k+m) < k·m. */
+int runlora_param_reduction(const runlora_shape_t* s);
+/* Bytes of device workspace that runlora_forward(fwd) and runlora_backward(bwd)
+ * (and the split _params/_input pair) need for shape s.  fwd or bwd may be 0 to
+ * size only the other.  The same workspace may be reused across calls. */
+runlora_status_t runlora_workspace_size(const runlora_shape_t* s, int fwd, int bwd, size_t* bytes);
+
+/* ---------------------------------------------------------------- selector
+ * RUNLORA_BY_FLOPS: argmin of Table 1 over {F1,F2} and {B1..B5}, ties to the
+ *   lowest index ("with flops criterion").  `ops`, workspace, stream unused.
+ * RUNLORA_BY_TIME: every executable candidate is run on `ops` on `stream`
+ *   (3 warm-ups, 15 timed reps each, CUDA events, median); forward and backward
+ *   timed independently; argmin of the medians.  Needs a workspace of
+ *   runlora_workspace_size(s, 2, 4) bytes or more (the largest candidate set).
+ *   Blocks the calling thread until timing is done.
+ * RUNLORA_HYBRID: as TIME but only candidates within 2x of the FLOP minimum.
+ * The FLOP pick is always reported in flops_*_pick.  Plans are cached in the
+ * handle per (shape, criterion). */
+runlora_status_t runlora_select(runlora_handle_t h, const runlora_shape_t* s, int criterion,
+                                const runlora_operands_t* ops, void* workspace, size_t ws_bytes,
+                                void* stream, runlora_plan_t* out);
+
+/* ----------------------------------------------------------------- execute
+ * Y[n,m] is overwritten.  fwd in {1,2}. */
+runlora_status_t runlora_forward(runlora_handle_t h, int fwd, const runlora_shape_t* s,
+                                 const void* X, const void* W, const void* A, const void* B, void* Y,
+                                 void* workspace, size_t ws_bytes, void* stream);
+
+/* dX[n,k] (nullable: skipped), dA[k,r], dB[r,m].  bwd in {1..5}.
+ * grad_dtype: dtype of dA/dB (RUNLORA_F32 or RUNLORA_BF16; must be RUNLORA_F32
+ * when s->dtype is RUNLORA_F32).  accumulate != 0 adds into dA/dB instead of
+ * overwriting (micro-batch accumulation); dA/dB are reduced over all n tokens in
+ * fp32 before the single rounding to grad_dtype. */
+runlora_status_t runlora_backward(runlora_handle_t h, int bwd, const runlora_shape_t* s,
+                                  const void* X, const void* W, const void* A, const void* B,
+                                  const void* dY, void* dX, void* dA, void* dB, int grad_dtype,
+                                  int accumulate, void* workspace, size_t ws_bytes, void* stream);
+
+/* Split backward for data-parallel overlap: _params computes dA, dB (and, for
+ * backward1..3, leaves Z1 = dY·Bᵀ in the workspace); _input computes dX and must
+ * follow the _params call of the same variant/shape with the same workspace on
+ * the same stream.  runlora_backward == _params then _input. */
+runlora_status_t runlora_backward_params(runlora_handle_t h, int bwd, const runlora_shape_t* s,
+                                         const void* X, const void* W, const void* A, const void* B,
+                                         const void* dY, void* dA, void* dB, int grad_dtype, int accumulate,
+                                         void* workspace, size_t ws_bytes, void* stream);
+runlora_status_t runlora_backward_input(runlora_handle_t h, int bwd, const runlora_shape_t* s,
+                                        const void* X, const void* W, const void* A, const void* B,
+                                        const void* dY, void* dX, void* workspace, size_t ws_bytes,
+                                        void* stream);
+
+/* End-to-end step from HOST buffers: H2D copies of X_host and dY_host into the
+ * device staging buffers X, dY; forward(fwd) into Y; backward(bwd) into dX, dA,
+ * dB; D2H copies of dA, dB into dA_host, dB_host (and of Y / dX when Y_host /
+ * dX_host are non-NULL).  Everything is enqueued on `stream`; the call returns
+ * without synchronising.  W, A, B are device pointers (resident parameters). */
+typedef struct {
+  int32_t fwd, bwd, grad_dtype, accumulate;
+  const void *X_host, *dY_host;          /* host inputs  */
+  void *Y_host, *dX_host;                /* host outputs, nullable */
+  void *dA_host, *dB_host;               /* host outputs */
+  const void *W, *A, *B;                 /* device parameters */
+  void *X, *dY, *Y, *dX, *dA, *dB;       /* device staging buffers */
+} runlora_host_step_t;
+runlora_status_t runlora_step_host(runlora_handle_t h, const runlora_shape_t* s, const runlora_host_step_t* st,
+                                   void* workspace, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- tracing
+ * When enabled, every kernel the library launches is bracketed by CUDA events
+ * on its stream; runlora_profile_read synchronises those events and returns
+ * per-kernel totals (and resets them when reset != 0). */
+runlora_status_t runlora_profile_enable(runlora_handle_t h, int enable);
+runlora_status_t runlora_profile_read(runlora_handle_t h, runlora_kernel_stat_t* stats, int max_stats,
+                                      int* count, int reset);
+/* Number of kernels this handle has launched since creation. */
+uint64_t runlora_launch_count(runlora_handle_t h);
+
+const char* runlora_status_string(runlora_status_t st);
+const char* runlora_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RUNLORA_H_ */

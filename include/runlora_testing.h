@@ -1,0 +1,30 @@
+/*
+ * runlora_testing.h — test hook of librunlora.so (not part of the stable ABI).
+ *
+ * runlora_debug_gemm runs ONE launch of the library's tcgen05 GEMM kernel
+ * (the building block of every bf16 product of Eq. 1-3 / Alg. 1-5, PAPER.md
+ * P:42-154) so that each operand-majorness / tile-width / split / epilogue
+ * combination can be checked in isolation:
+ *
+ *   D[M,N] = A1·B1 (+ A2·B2)   bf16 operands, fp32 accumulation
+ *   A1: a_mn == 0 -> stored [M, K1] row-major; a_mn == 1 -> stored [K1, M]
+ *   B1: b_mn == 0 -> stored [N, K1] row-major; b_mn == 1 -> stored [K1, N]
+ *   A2/B2: same majors with K2 (K2 == 0: no tail)
+ *   out_mode 0: D bf16 [M, N]; 1: D bf16 = acc + Cin (bf16 [M, N]);
+ *            2: D fp32 partial slabs [splits][M][N] (split-K over K1)
+ *   BN: tile width (16, 32, 48, 64, 128, 256; MN-major B needs a multiple of 64).
+ * All pointers are device pointers; rows are contiguous (ld = number of columns).
+ */
+#ifndef RUNLORA_TESTING_H_
+#define RUNLORA_TESTING_H_
+#include "runlora.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+runlora_status_t runlora_debug_gemm(runlora_handle_t h, int M, int N, int K1, const void* A1, int a_mn,
+                                    const void* B1, int b_mn, int K2, const void* A2, const void* B2, int out_mode,
+                                    void* D, const void* Cin, int BN, int splits, void* stream);
+#ifdef __cplusplus
+}
+#endif
+#endif

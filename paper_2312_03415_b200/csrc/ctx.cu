@@ -1,0 +1,138 @@
+// Per-handle host context: device facts, TMA descriptor cache, launch counting
+// and CUDA-event kernel profiling.
+#include <cstdio>
+#include <cstring>
+
+#include "internal.h"
+
+namespace runlora {
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+Ctx::Ctx(int device) : device_(device) {
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0) num_sms_ = sms;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    encode_fn_ = fn;
+}
+
+Ctx::~Ctx() {
+  for (auto& p : pending_) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : free_events_) cudaEventDestroy(e);
+  if (cur_start_) cudaEventDestroy(cur_start_);
+}
+
+bool Ctx::tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* err) {
+  char key[160];
+  snprintf(key, sizeof key, "%p/%lld/%lld/%lld/%d", m.ptr, (long long)m.rows, (long long)m.cols, (long long)m.ld,
+           box_rows);
+  {
+    std::lock_guard<std::mutex> g(tmap_mu_);
+    auto it = tmaps_.find(key);
+    if (it != tmaps_.end()) {
+      *out = it->second;
+      return true;
+    }
+  }
+  if (!encode_fn_) {
+    if (err) *err = "cuTensorMapEncodeTiled entry point unavailable";
+    return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)m.cols, (cuuint64_t)m.rows};
+  cuuint64_t strides[1] = {(cuuint64_t)m.ld * 2};
+  cuuint32_t box[2] = {64u, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUtensorMap tm;
+  CUresult r = reinterpret_cast<EncodeTiledFn>(encode_fn_)(
+      &tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(m.ptr), dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    if (err) {
+      char buf[256];
+      snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d) for %lldx%lld ld=%lld box=64x%d ptr=%p", (int)r,
+               (long long)m.rows, (long long)m.cols, (long long)m.ld, box_rows, m.ptr);
+      *err = buf;
+    }
+    return false;
+  }
+  std::lock_guard<std::mutex> g(tmap_mu_);
+  if (tmaps_.size() > 4096) tmaps_.clear();
+  tmaps_[key] = tm;
+  *out = tm;
+  return true;
+}
+
+cudaEvent_t Ctx::get_event() {
+  if (!free_events_.empty()) {
+    cudaEvent_t e = free_events_.back();
+    free_events_.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void Ctx::launch_begin(cudaStream_t s, KernelId kid) {
+  ++launches_;
+  if (!profiling_) return;
+  cur_kid_ = kid;
+  cur_start_ = get_event();
+  cudaEventRecord(cur_start_, s);
+}
+
+void Ctx::launch_end(cudaStream_t s) {
+  if (!profiling_ || !cur_start_) return;
+  cudaEvent_t b = get_event();
+  cudaEventRecord(b, s);
+  pending_.push_back({cur_kid_, cur_start_, b});
+  cur_start_ = nullptr;
+}
+
+void Ctx::profile_enable(bool on) { profiling_ = on; }
+
+bool Ctx::profile_read(runlora_kernel_stat_t* stats, int max_stats, int* count, bool reset, std::string* err) {
+  for (auto& p : pending_) {
+    if (cudaEventSynchronize(p.b) != cudaSuccess) {
+      if (err) *err = "cudaEventSynchronize failed while reading profile";
+      return false;
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    stat_launches_[p.kid] += 1;
+    stat_ms_[p.kid] += ms;
+    free_events_.push_back(p.a);
+    free_events_.push_back(p.b);
+  }
+  pending_.clear();
+  int n = 0;
+  for (int k = 0; k < KID_COUNT; ++k) {
+    if (stat_launches_[k] == 0) continue;
+    if (stats && n < max_stats) {
+      memset(&stats[n], 0, sizeof(stats[n]));
+      strncpy(stats[n].name, kKernelNames[k], sizeof(stats[n].name) - 1);
+      stats[n].launches = stat_launches_[k];
+      stats[n].total_ms = stat_ms_[k];
+    }
+    ++n;
+  }
+  if (count) *count = n;
+  if (reset) {
+    for (int k = 0; k < KID_COUNT; ++k) {
+      stat_launches_[k] = 0;
+      stat_ms_[k] = 0.0;
+    }
+  }
+  return true;
+}
+
+}  // namespace runlora

@@ -1,0 +1,111 @@
+// Internal interfaces between the ABI layer (runlora.cu) and the kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/runlora.h"
+
+namespace runlora {
+
+// Kernel identities for launch counting / profiling.
+enum KernelId : int {
+  KID_GEMM_MAIN = 0,   // Y / dX GEMMs (dominant, tensor-bound)
+  KID_GEMM_WPRIME,     // W + A·B (rank-r update, HBM-bound)
+  KID_GEMM_PROJ,       // X·A, dY·Bᵀ (rank-r projections, HBM-bound)
+  KID_GEMM_TOKRED,     // Xᵀ·Z1, dYᵀ·Z2 (token reductions, HBM-bound)
+  KID_GEMM_DENSE_XTDY, // Xᵀ·dY (backward2..4 dense intermediate)
+  KID_GEMM_SMALL,      // Z2'·Bᵀ, Z2'ᵀ·A (backward3/4 adapter grads)
+  KID_SPLITK_REDUCE,   // fixed-order split-K reduction / cast / transpose
+  KID_SGEMM_F32,       // fp32 SIMT GEMM (RUNLORA_F32 path)
+  KID_COUNT
+};
+extern const char* const kKernelNames[KID_COUNT];
+
+struct DeviceMat {  // row-major bf16 matrix view: element (i, j) at ptr[i*ld + j]
+  const void* ptr;
+  int64_t rows, cols, ld;
+};
+
+struct GemmReq {
+  int M, N;
+  DeviceMat a;
+  bool a_mn;       // false: a stored [M, K] (K-major); true: a stored [K, M] (MN-major)
+  DeviceMat b;
+  bool b_mn;       // false: b stored [N, K] (K-major); true: b stored [K, N] (MN-major)
+  int K1;
+  DeviceMat a2, b2;  // concat-K tail (same majors); K2 == 0: none
+  int K2;
+  int out_mode;      // OutMode
+  void* D;
+  int64_t ldd;
+  int64_t split_stride;
+  const void* Cin;
+  int64_t ldc;
+  int BN;
+  int splits;        // >= 1 (only with OUT_F32)
+  int kb_per_split;
+  bool a_stream_once;  // A operand is read once (evict-first hint)
+  KernelId kid;
+};
+
+class Ctx {
+ public:
+  explicit Ctx(int device);
+  ~Ctx();
+  int device() const { return device_; }
+  int num_sms() const { return num_sms_; }
+
+  // Encodes (or fetches from cache) a 2-D bf16 TMA descriptor with 128B swizzle:
+  // dims {cols, rows}, row stride ld*2 bytes, box {64, box_rows}.
+  bool tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* err);
+
+  // Profiling hooks around every launch.
+  void launch_begin(cudaStream_t s, KernelId kid);
+  void launch_end(cudaStream_t s);
+  void profile_enable(bool on);
+  bool profile_read(runlora_kernel_stat_t* stats, int max_stats, int* count, bool reset, std::string* err);
+  uint64_t launches() const { return launches_; }
+
+  std::mutex plan_mu;
+  std::map<std::vector<int64_t>, runlora_plan_t> plans;
+
+ private:
+  int device_;
+  int num_sms_ = 148;
+  void* encode_fn_ = nullptr;
+  std::mutex tmap_mu_;
+  std::unordered_map<std::string, CUtensorMap> tmaps_;
+  bool profiling_ = false;
+  uint64_t launches_ = 0;
+  struct Pending {
+    KernelId kid;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending_;
+  std::vector<cudaEvent_t> free_events_;
+  KernelId cur_kid_ = KID_GEMM_MAIN;
+  cudaEvent_t cur_start_ = nullptr;
+  uint64_t stat_launches_[KID_COUNT] = {};
+  double stat_ms_[KID_COUNT] = {};
+  cudaEvent_t get_event();
+};
+
+// Kernel launchers (kernels.cu). Return cudaSuccess or the launch error.
+cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq& r, cudaStream_t s, std::string* err);
+cudaError_t launch_splitk_reduce(Ctx& ctx, const float* P, int splits, int64_t split_stride, int rows, int cols,
+                                 int64_t ldp, void* out, bool out_bf16, int64_t ldo, bool transpose,
+                                 bool accumulate, cudaStream_t s);
+// fp32 SIMT GEMM: C[i,j] = (acc ? C[i,j] : 0) + (Cadd ? Cadd[i,j] : 0) + sum_t A(i,t) B(t,j),
+// A(i,t) = A[i*sa0 + t*sa1], B(t,j) = B[t*sb0 + j*sb1].
+cudaError_t launch_sgemm(Ctx& ctx, int M, int N, int K, const float* A, int64_t sa0, int64_t sa1, const float* B,
+                         int64_t sb0, int64_t sb1, float* C, int64_t ldc, const float* Cadd, int64_t ldadd,
+                         bool accumulate, cudaStream_t s);
+
+}  // namespace runlora

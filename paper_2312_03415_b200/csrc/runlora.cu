@@ -1,0 +1,808 @@
+// C ABI of the RunLoRA hot path (include/runlora.h): validation, Table 1 cost
+// model, selector, and the launch sequence of every forward/backward variant.
+//
+// Variant sequences (bf16; every product is one tcgen05 launch, see tc_gemm.cuh):
+//   forward1:  Z2 = X·A                      [proj, split-K -> reduce -> bf16]
+//                     Y  = [X | Z2]·[W ; B]         [main GEMM, concat-K tail]
+//   forward2:  W' = W + A·B                  [K = r, epilogue adds W, bf16]
+//                     Y  = X·W'                     [main GEMM]
+//   backward1 (Alg.1): Z1 = dY·Bᵀ; Z2 = X·A; dA = Xᵀ·Z1; dB = Z2ᵀ·dY;
+//                     dX = [dY | Z1]·[Wᵀ ; Aᵀ]
+//   backward2 (Alg.2): Z1; Z2' = Xᵀ·dY; dA = Xᵀ·Z1; dB = Aᵀ·Z2'; dX as B1
+//   backward3 (Alg.3): Z1; Z2'; dA = Z2'·Bᵀ; dB = Aᵀ·Z2'; dX as B1
+//   backward4 (Alg.4): Z2'; dA = Z2'·Bᵀ; dB = Aᵀ·Z2'; W' = W+AB; dX = dY·W'ᵀ
+//   backward5 (Alg.5): Z1; Z2; dA = Xᵀ·Z1; dB = Z2ᵀ·dY; W' = W+AB; dX = dY·W'ᵀ
+// dB is produced as dBᵀ = (·)ᵀ·(·) so that the rank sits on the MMA's N axis and is
+// transposed by the split-K reducer.  fp32 (RUNLORA_F32) runs the same algorithm
+// lines with the fp32 SIMT GEMM (true FFMA; the 1e-5 tolerance excludes TF32).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <algorithm>
+
+#include "internal.h"
+#include "tc_gemm.cuh"
+
+using namespace runlora;
+
+struct runlora_handle_s {
+  Ctx* ctx;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+runlora_status_t fail(runlora_status_t st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+#define RL_TRY(expr)                       \
+  do {                                     \
+    runlora_status_t _st = (expr);         \
+    if (_st != RUNLORA_OK) return _st;     \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+bool mul_ok(unsigned __int128 v) { return v <= (unsigned __int128)UINT64_MAX; }
+
+runlora_status_t check_shape(const runlora_shape_t* s) {
+  if (!s) return fail(RUNLORA_ERR_INVALID_ARG, "shape is NULL");
+  if (s->n <= 0 || s->k <= 0 || s->m <= 0 || s->r <= 0) {
+    char b[160];
+    snprintf(b, sizeof b, "n, k, m, r must all be >= 1 (got n=%lld k=%lld m=%lld r=%lld)", (long long)s->n,
+             (long long)s->k, (long long)s->m, (long long)s->r);
+    return fail(RUNLORA_ERR_INVALID_ARG, b);
+  }
+  if (s->dtype != RUNLORA_F32 && s->dtype != RUNLORA_BF16) return fail(RUNLORA_ERR_DTYPE, "dtype must be F32 or BF16");
+  const int64_t lim = (int64_t)1 << 31;
+  if (s->n >= lim || s->k >= lim || s->m >= lim || s->r >= lim)
+    return fail(RUNLORA_ERR_INVALID_ARG, "each of n, k, m, r must be < 2^31");
+  if (s->dtype == RUNLORA_BF16 && ((s->k | s->m | s->r) & 7)) {
+    char b[160];
+    snprintf(b, sizeof b, "bf16 needs k, m, r multiples of 8 for 16-byte TMA row strides (k=%lld m=%lld r=%lld)",
+             (long long)s->k, (long long)s->m, (long long)s->r);
+    return fail(RUNLORA_ERR_ALIGNMENT, b);
+  }
+  return RUNLORA_OK;
+}
+
+runlora_status_t check_ptr(const void* p, const char* name, bool nullable = false) {
+  if (!p) {
+    if (nullable) return RUNLORA_OK;
+    return fail(RUNLORA_ERR_INVALID_ARG, std::string(name) + " is NULL");
+  }
+  if (reinterpret_cast<uintptr_t>(p) & 15) return fail(RUNLORA_ERR_ALIGNMENT, std::string(name) + " is not 16-byte aligned");
+  return RUNLORA_OK;
+}
+
+runlora_status_t cuda_fail(cudaError_t e, const char* what) {
+  char b[256];
+  snprintf(b, sizeof b, "%s: %s", what, cudaGetErrorString(e));
+  return fail(RUNLORA_ERR_CUDA, b);
+}
+
+// ------------------------------------------------------------ Table 1
+runlora_status_t flops_of(const runlora_shape_t* s, int is_backward, int v, uint64_t* out) {
+  typedef unsigned __int128 u;
+  const u n = (u)s->n, i = (u)s->k, o = (u)s->m, r = (u)s->r;
+  u f;
+  if (!is_backward) {
+    if (v == 1) f = 2 * n * (i * o + r * i + o * r);
+    else if (v == 2) f = 2 * (i * o * r + n * o * i);
+    else return fail(RUNLORA_ERR_INVALID_ARG, "forward variant must be 1 or 2 (P:62-64)");
+  } else {
+    switch (v) {
+      case 1: f = 2 * n * (2 * o * r + 3 * i * r + o * i); break;
+      case 2: f = 2 * n * (o * r + 2 * i * r + 2 * i * o) + 2 * i * o * r; break;
+      case 3: f = 2 * n * (2 * i * o + o * r + i * r) + 4 * i * r * o; break;
+      case 4: f = 2 * (2 * n * i * o + 3 * i * o * r); break;
+      case 5: f = 2 * n * (2 * o * r + 2 * i * r + o * i) + 2 * i * o * r; break;
+      case 6: f = 2 * n * (2 * o * r + 2 * i * r + 2 * o * i) + 4 * i * o * r; break;
+      case 7:
+      case 8: f = 2 * n * (o * r + i * r + 2 * o * i) + 4 * i * o * r; break;
+      default: return fail(RUNLORA_ERR_INVALID_ARG, "backward variant must be 1..8 (P:84-94)");
+    }
+  }
+  if (!mul_ok(f)) return fail(RUNLORA_ERR_OVERFLOW, "FLOP count exceeds uint64");
+  *out = (uint64_t)f;
+  return RUNLORA_OK;
+}
+
+// -------------------------------------------------------------- skinny plans
+constexpr int kSplitTargetUnits = 296;  // 2 x 148 SMs (fixed so workspace size is device-independent)
+constexpr int kMaxSplits = 16;
+
+struct SkinnyPlan {
+  int BN, Npad, splits, kps;
+};
+
+int round_bn_k(int64_t r) {  // K-major B: smallest legal UMMA N >= r (<= 256)
+  static const int opts[] = {16, 32, 48, 64, 128, 256};
+  for (int o : opts)
+    if (r <= o) return o;
+  return 256;
+}
+
+SkinnyPlan plan_skinny(int64_t rows, int64_t K, int64_t r, bool b_mn) {
+  SkinnyPlan p;
+  p.BN = b_mn ? (r <= 64 ? 64 : r <= 128 ? 128 : 256) : round_bn_k(r);
+  const int64_t ntn = (r + p.BN - 1) / p.BN;
+  p.Npad = (int)(ntn * p.BN);
+  const int64_t tiles = ((rows + kBM - 1) / kBM) * ntn;
+  const int64_t kblocks = (K + kBK - 1) / kBK;
+  int64_t s = (kSplitTargetUnits + tiles - 1) / tiles;
+  s = std::min<int64_t>(s, kMaxSplits);
+  s = std::min<int64_t>(s, std::max<int64_t>(1, kblocks / 2));
+  s = std::max<int64_t>(s, 1);
+  p.kps = (int)((kblocks + s - 1) / s);
+  p.splits = (int)((kblocks + p.kps - 1) / p.kps);
+  return p;
+}
+
+size_t partial_bytes(int64_t rows, int64_t K, int64_t r, bool b_mn) {
+  SkinnyPlan p = plan_skinny(rows, K, r, b_mn);
+  return (size_t)p.splits * (size_t)rows * (size_t)p.Npad * 4;
+}
+
+// ------------------------------------------------------------ workspace layout
+struct Layout {
+  size_t z1, z2, wp, p, total;
+};
+size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+Layout layout_of(const runlora_shape_t& s) {
+  const size_t es = s.dtype == RUNLORA_BF16 ? 2 : 4;
+  const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
+  Layout L;
+  L.z1 = 0;
+  L.z2 = al((size_t)n * r * es);
+  L.wp = L.z2 + al((size_t)n * r * es);
+  L.p = L.wp + al((size_t)k * m * es);
+  size_t pb = 0;
+  if (s.dtype == RUNLORA_BF16) {
+    pb = std::max(pb, partial_bytes(n, k, r, true));    // Z2 = X·A
+    pb = std::max(pb, partial_bytes(n, m, r, false));   // Z1 = dY·Bᵀ
+    pb = std::max(pb, partial_bytes(k, n, r, true));    // dA = Xᵀ·Z1
+    pb = std::max(pb, partial_bytes(m, n, r, true));    // dBᵀ = dYᵀ·Z2
+    pb = std::max(pb, partial_bytes(k, m, r, false));   // dA = Z2'·Bᵀ
+    pb = std::max(pb, partial_bytes(m, k, r, true));    // dBᵀ = Z2'ᵀ·A
+  }
+  L.total = L.p + al(pb);
+  return L;
+}
+
+struct Bufs {
+  void *z1, *z2, *wp;
+  float* P;
+};
+
+runlora_status_t bind_ws(const runlora_shape_t& s, void* ws, size_t ws_bytes, Bufs* b) {
+  Layout L = layout_of(s);
+  if (!ws) return fail(RUNLORA_ERR_INVALID_ARG, "workspace is NULL");
+  if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(RUNLORA_ERR_ALIGNMENT, "workspace must be 256-byte aligned");
+  if (ws_bytes < L.total) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "workspace too small: %zu bytes given, %zu needed", ws_bytes, L.total);
+    return fail(RUNLORA_ERR_WORKSPACE, buf);
+  }
+  char* base = static_cast<char*>(ws);
+  b->z1 = base + L.z1;
+  b->z2 = base + L.z2;
+  b->wp = base + L.wp;
+  b->P = reinterpret_cast<float*>(base + L.p);
+  return RUNLORA_OK;
+}
+
+DeviceMat mat(const void* p, int64_t rows, int64_t cols) { return DeviceMat{p, rows, cols, cols}; }
+
+runlora_status_t gemm(Ctx& c, const GemmReq& q, cudaStream_t st) {
+  std::string err;
+  cudaError_t e = launch_tc_gemm(c, q, st, &err);
+  if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
+  return RUNLORA_OK;
+}
+
+GemmReq base_req(int M, int N, KernelId kid) {
+  GemmReq q;
+  memset(&q, 0, sizeof q);
+  q.M = M;
+  q.N = N;
+  q.splits = 1;
+  q.kid = kid;
+  return q;
+}
+
+// out = A_op[rows, K]·B_op[K, r]: fp32 split-K partials, then a fixed-order reduce
+// that casts (and optionally transposes / accumulates) into `out`.
+runlora_status_t skinny(Ctx& c, DeviceMat a, bool a_mn, DeviceMat b, bool b_mn, int64_t rows, int64_t K, int64_t r,
+                        void* out, bool out_bf16, int64_t ldo, bool transpose, bool accumulate, float* P,
+                        KernelId kid, cudaStream_t st) {
+  SkinnyPlan p = plan_skinny(rows, K, r, b_mn);
+  GemmReq q = base_req((int)rows, p.Npad, kid);
+  q.a = a;
+  q.a_mn = a_mn;
+  q.b = b;
+  q.b_mn = b_mn;
+  q.K1 = (int)K;
+  q.out_mode = OUT_F32;
+  q.D = P;
+  q.ldd = p.Npad;
+  q.split_stride = rows * (int64_t)p.Npad;
+  q.BN = p.BN;
+  q.splits = p.splits;
+  q.kb_per_split = p.kps;
+  q.a_stream_once = true;
+  RL_TRY(gemm(c, q, st));
+  cudaError_t e = launch_splitk_reduce(c, P, p.splits, q.split_stride, (int)rows, (int)r, p.Npad, out, out_bf16, ldo,
+                                       transpose, accumulate, st);
+  if (e != cudaSuccess) return cuda_fail(e, "splitk_reduce launch");
+  return RUNLORA_OK;
+}
+
+// W' = W + A·B  (k×m, bf16, formed in fp32 in TMEM and rounded once).
+runlora_status_t wprime_bf16(Ctx& c, const runlora_shape_t& s, const void* W, const void* A, const void* B, void* Wp,
+                             cudaStream_t st) {
+  GemmReq q = base_req((int)s.k, (int)s.m, KID_GEMM_WPRIME);
+  q.a = mat(A, s.k, s.r);  // A_op[M=k, K=r], K-major
+  q.a_mn = false;
+  q.b = mat(B, s.r, s.m);  // B_op[K=r, N=m] stored [K, N]: MN-major
+  q.b_mn = true;
+  q.K1 = (int)s.r;
+  q.out_mode = OUT_BF16_ADD;
+  q.Cin = W;
+  q.ldc = s.m;
+  q.D = Wp;
+  q.ldd = s.m;
+  q.BN = 256;
+  return gemm(c, q, st);
+}
+
+// ------------------------------------------------------------ bf16 variants
+runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* X, const void* W, const void* A,
+                              const void* B, void* Y, Bufs& b, cudaStream_t st) {
+  const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
+  GemmReq q = base_req((int)n, (int)m, KID_GEMM_MAIN);
+  q.a = mat(X, n, k);
+  q.a_mn = false;
+  q.K1 = (int)k;
+  q.b_mn = true;
+  q.out_mode = OUT_BF16;
+  q.D = Y;
+  q.ldd = m;
+  q.BN = 256;
+  if (v == 1) {
+    // Z2 = X·A (never saved for the backward)
+    RL_TRY(skinny(c, mat(X, n, k), false, mat(A, k, r), true, n, k, r, b.z2, true, r, false, false, b.P,
+                  KID_GEMM_PROJ, st));
+    q.b = mat(W, k, m);
+    q.a2 = mat(b.z2, n, r);
+    q.b2 = mat(B, r, m);
+    q.K2 = (int)r;
+  } else {
+    RL_TRY(wprime_bf16(c, s, W, A, B, b.wp, st));
+    q.b = mat(b.wp, k, m);
+  }
+  return gemm(c, q, st);
+}
+
+runlora_status_t params_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* X, const void* A, const void* B,
+                             const void* dY, void* dA, void* dB, bool g_bf16, bool acc, Bufs& b, cudaStream_t st) {
+  const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
+  const bool need_z1 = v == 1 || v == 2 || v == 3 || v == 5;
+  const bool need_z2 = v == 1 || v == 5;
+  const bool dense = v == 2 || v == 3 || v == 4;
+  if (need_z1)  // Z1 = dY·Bᵀ: B_op[K=m, N=r] = Bᵀ, stored [N, K] = B -> K-major
+    RL_TRY(skinny(c, mat(dY, n, m), false, mat(B, r, m), false, n, m, r, b.z1, true, r, false, false, b.P,
+                  KID_GEMM_PROJ, st));
+  if (need_z2)  // Z2 = X·A
+    RL_TRY(skinny(c, mat(X, n, k), false, mat(A, k, r), true, n, k, r, b.z2, true, r, false, false, b.P,
+                  KID_GEMM_PROJ, st));
+  if (dense) {  // Z2' = Xᵀ·dY (k×m): A_op = Xᵀ (MN-major X), B_op = dY (MN-major)
+    GemmReq q = base_req((int)k, (int)m, KID_GEMM_DENSE_XTDY);
+    q.a = mat(X, n, k);
+    q.a_mn = true;
+    q.b = mat(dY, n, m);
+    q.b_mn = true;
+    q.K1 = (int)n;
+    q.out_mode = OUT_BF16;
+    q.D = b.wp;
+    q.ldd = m;
+    q.BN = 256;
+    RL_TRY(gemm(c, q, st));
+  }
+  // dA
+  if (v == 1 || v == 2 || v == 5)  // dA = Xᵀ·Z1 (token reduction, K = n)
+    RL_TRY(skinny(c, mat(X, n, k), true, mat(b.z1, n, r), true, k, n, r, dA, g_bf16, r, false, acc, b.P,
+                  KID_GEMM_TOKRED, st));
+  else  // dA = Z2'·Bᵀ
+    RL_TRY(skinny(c, mat(b.wp, k, m), false, mat(B, r, m), false, k, m, r, dA, g_bf16, r, false, acc, b.P,
+                  KID_GEMM_SMALL, st));
+  // dB (as dBᵀ[m, r], transposed by the reducer into dB[r, m])
+  if (v == 1 || v == 5)  // dBᵀ = dYᵀ·Z2
+    RL_TRY(skinny(c, mat(dY, n, m), true, mat(b.z2, n, r), true, m, n, r, dB, g_bf16, m, true, acc, b.P,
+                  KID_GEMM_TOKRED, st));
+  else  // dBᵀ = Z2'ᵀ·A
+    RL_TRY(skinny(c, mat(b.wp, k, m), true, mat(A, k, r), true, m, k, r, dB, g_bf16, m, true, acc, b.P,
+                  KID_GEMM_SMALL, st));
+  return RUNLORA_OK;
+}
+
+runlora_status_t input_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* W, const void* A, const void* B,
+                            const void* dY, void* dX, Bufs& b, cudaStream_t st) {
+  const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
+  GemmReq q = base_req((int)n, (int)k, KID_GEMM_MAIN);
+  q.a = mat(dY, n, m);
+  q.a_mn = false;
+  q.b_mn = false;
+  q.K1 = (int)m;
+  q.out_mode = OUT_BF16;
+  q.D = dX;
+  q.ldd = k;
+  q.BN = 256;
+  if (v <= 3) {  // dX = [dY | Z1]·[Wᵀ ; Aᵀ]
+    q.b = mat(W, k, m);  // B_op[K=m, N=k] = Wᵀ stored [N, K] = W: K-major
+    q.a2 = mat(b.z1, n, r);
+    q.b2 = mat(A, k, r);  // Aᵀ stored [N=k, K=r] = A: K-major
+    q.K2 = (int)r;
+  } else {  // dX = dY·W'ᵀ
+    RL_TRY(wprime_bf16(c, s, W, A, B, b.wp, st));
+    q.b = mat(b.wp, k, m);
+  }
+  return gemm(c, q, st);
+}
+
+// ------------------------------------------------------------ fp32 variants
+runlora_status_t sg(Ctx& c, int M, int N, int K, const void* A, int64_t sa0, int64_t sa1, const void* B, int64_t sb0,
+                    int64_t sb1, void* C, int64_t ldc, const void* Cadd, int64_t ldadd, bool acc, cudaStream_t st) {
+  cudaError_t e = launch_sgemm(c, M, N, K, (const float*)A, sa0, sa1, (const float*)B, sb0, sb1, (float*)C, ldc,
+                               (const float*)Cadd, ldadd, acc, st);
+  if (e != cudaSuccess) return cuda_fail(e, "sgemm launch");
+  return RUNLORA_OK;
+}
+
+runlora_status_t forward_f32(Ctx& c, int v, const runlora_shape_t& s, const void* X, const void* W, const void* A,
+                             const void* B, void* Y, Bufs& b, cudaStream_t st) {
+  const int n = (int)s.n, k = (int)s.k, m = (int)s.m, r = (int)s.r;
+  if (v == 1) {
+    RL_TRY(sg(c, n, r, k, X, k, 1, A, r, 1, b.z2, r, nullptr, 0, false, st));   // Z2 = X·A
+    RL_TRY(sg(c, n, m, k, X, k, 1, W, m, 1, Y, m, nullptr, 0, false, st));      // Y = X·W
+    return sg(c, n, m, r, b.z2, r, 1, B, m, 1, Y, m, nullptr, 0, true, st);    // Y += Z2·B
+  }
+  RL_TRY(sg(c, k, m, r, A, r, 1, B, m, 1, b.wp, m, W, m, false, st));         // W' = W + A·B
+  return sg(c, n, m, k, X, k, 1, b.wp, m, 1, Y, m, nullptr, 0, false, st);     // Y = X·W'
+}
+
+runlora_status_t params_f32(Ctx& c, int v, const runlora_shape_t& s, const void* X, const void* A, const void* B,
+                            const void* dY, void* dA, void* dB, bool acc, Bufs& b, cudaStream_t st) {
+  const int n = (int)s.n, k = (int)s.k, m = (int)s.m, r = (int)s.r;
+  if (v == 1 || v == 2 || v == 3 || v == 5)
+    RL_TRY(sg(c, n, r, m, dY, m, 1, B, 1, m, b.z1, r, nullptr, 0, false, st));  // Z1 = dY·Bᵀ
+  if (v == 1 || v == 5) RL_TRY(sg(c, n, r, k, X, k, 1, A, r, 1, b.z2, r, nullptr, 0, false, st));  // Z2 = X·A
+  if (v == 2 || v == 3 || v == 4)
+    RL_TRY(sg(c, k, m, n, X, 1, k, dY, m, 1, b.wp, m, nullptr, 0, false, st));  // Z2' = Xᵀ·dY
+  if (v == 1 || v == 2 || v == 5)
+    RL_TRY(sg(c, k, r, n, X, 1, k, b.z1, r, 1, dA, r, nullptr, 0, acc, st));     // dA = Xᵀ·Z1
+  else
+    RL_TRY(sg(c, k, r, m, b.wp, m, 1, B, 1, m, dA, r, nullptr, 0, acc, st));     // dA = Z2'·Bᵀ
+  if (v == 1 || v == 5)
+    RL_TRY(sg(c, r, m, n, b.z2, 1, r, dY, m, 1, dB, m, nullptr, 0, acc, st));    // dB = Z2ᵀ·dY
+  else
+    RL_TRY(sg(c, r, m, k, A, 1, r, b.wp, m, 1, dB, m, nullptr, 0, acc, st));     // dB = Aᵀ·Z2'
+  return RUNLORA_OK;
+}
+
+runlora_status_t input_f32(Ctx& c, int v, const runlora_shape_t& s, const void* W, const void* A, const void* B,
+                           const void* dY, void* dX, Bufs& b, cudaStream_t st) {
+  const int n = (int)s.n, k = (int)s.k, m = (int)s.m, r = (int)s.r;
+  if (v <= 3) {
+    RL_TRY(sg(c, n, k, m, dY, m, 1, W, 1, m, dX, k, nullptr, 0, false, st));   // dX = dY·Wᵀ
+    return sg(c, n, k, r, b.z1, r, 1, A, 1, r, dX, k, nullptr, 0, true, st);   // dX += Z1·Aᵀ
+  }
+  RL_TRY(sg(c, k, m, r, A, r, 1, B, m, 1, b.wp, m, W, m, false, st));        // W' = W + A·B
+  return sg(c, n, k, m, dY, m, 1, b.wp, 1, m, dX, k, nullptr, 0, false, st);  // dX = dY·W'ᵀ
+}
+
+// ------------------------------------------------------------ entry helpers
+runlora_status_t check_handle(runlora_handle_t h) {
+  if (!h || !h->ctx) return fail(RUNLORA_ERR_INVALID_ARG, "handle is NULL");
+  return RUNLORA_OK;
+}
+
+runlora_status_t post_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return RUNLORA_OK;
+}
+
+runlora_status_t do_forward(runlora_handle_t h, int fwd, const runlora_shape_t* s, const void* X, const void* W,
+                            const void* A, const void* B, void* Y, void* ws, size_t ws_bytes, void* stream) {
+  RL_TRY(check_handle(h));
+  RL_TRY(check_shape(s));
+  if (fwd != 1 && fwd != 2) return fail(RUNLORA_ERR_INVALID_ARG, "forward variant must be 1 or 2 (P:62-64)");
+  RL_TRY(check_ptr(X, "X"));
+  RL_TRY(check_ptr(W, "W"));
+  RL_TRY(check_ptr(A, "A"));
+  RL_TRY(check_ptr(B, "B"));
+  RL_TRY(check_ptr(Y, "Y"));
+  Bufs b;
+  RL_TRY(bind_ws(*s, ws, ws_bytes, &b));
+  DeviceGuard dg(h->ctx->device());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (s->dtype == RUNLORA_BF16) RL_TRY(forward_bf16(*h->ctx, fwd, *s, X, W, A, B, Y, b, st));
+  else RL_TRY(forward_f32(*h->ctx, fwd, *s, X, W, A, B, Y, b, st));
+  return post_launch();
+}
+
+runlora_status_t check_bwd_common(runlora_handle_t h, int bwd, const runlora_shape_t* s) {
+  RL_TRY(check_handle(h));
+  RL_TRY(check_shape(s));
+  if (bwd >= 6 && bwd <= 8)
+    return fail(RUNLORA_ERR_UNSUPPORTED_VARIANT,
+                "backward6..8 are cost-model only: the paper implements only the first five (P:96-98)");
+  if (bwd < 1 || bwd > 8) return fail(RUNLORA_ERR_INVALID_ARG, "backward variant must be 1..5");
+  return RUNLORA_OK;
+}
+
+runlora_status_t do_params(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X, const void* W,
+                           const void* A, const void* B, const void* dY, void* dA, void* dB, int grad_dtype,
+                           int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  RL_TRY(check_bwd_common(h, bwd, s));
+  (void)W;
+  RL_TRY(check_ptr(X, "X"));
+  RL_TRY(check_ptr(A, "A"));
+  RL_TRY(check_ptr(B, "B"));
+  RL_TRY(check_ptr(dY, "dY"));
+  RL_TRY(check_ptr(dA, "dA"));
+  RL_TRY(check_ptr(dB, "dB"));
+  if (grad_dtype != RUNLORA_F32 && grad_dtype != RUNLORA_BF16) return fail(RUNLORA_ERR_DTYPE, "grad_dtype must be F32 or BF16");
+  if (s->dtype == RUNLORA_F32 && grad_dtype != RUNLORA_F32)
+    return fail(RUNLORA_ERR_DTYPE, "fp32 operands need fp32 adapter gradients");
+  Bufs b;
+  RL_TRY(bind_ws(*s, ws, ws_bytes, &b));
+  DeviceGuard dg(h->ctx->device());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (s->dtype == RUNLORA_BF16)
+    RL_TRY(params_bf16(*h->ctx, bwd, *s, X, A, B, dY, dA, dB, grad_dtype == RUNLORA_BF16, accumulate != 0, b, st));
+  else
+    RL_TRY(params_f32(*h->ctx, bwd, *s, X, A, B, dY, dA, dB, accumulate != 0, b, st));
+  return post_launch();
+}
+
+runlora_status_t do_input(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* W, const void* A,
+                          const void* B, const void* dY, void* dX, void* ws, size_t ws_bytes, void* stream) {
+  RL_TRY(check_bwd_common(h, bwd, s));
+  RL_TRY(check_ptr(W, "W"));
+  RL_TRY(check_ptr(A, "A"));
+  RL_TRY(check_ptr(B, "B"));
+  RL_TRY(check_ptr(dY, "dY"));
+  RL_TRY(check_ptr(dX, "dX"));
+  Bufs b;
+  RL_TRY(bind_ws(*s, ws, ws_bytes, &b));
+  DeviceGuard dg(h->ctx->device());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (s->dtype == RUNLORA_BF16) RL_TRY(input_bf16(*h->ctx, bwd, *s, W, A, B, dY, dX, b, st));
+  else RL_TRY(input_f32(*h->ctx, bwd, *s, W, A, B, dY, dX, b, st));
+  return post_launch();
+}
+
+runlora_status_t do_backward(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X, const void* W,
+                             const void* A, const void* B, const void* dY, void* dX, void* dA, void* dB,
+                             int grad_dtype, int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  RL_TRY(do_params(h, bwd, s, X, W, A, B, dY, dA, dB, grad_dtype, accumulate, ws, ws_bytes, stream));
+  if (dX) RL_TRY(do_input(h, bwd, s, W, A, B, dY, dX, ws, ws_bytes, stream));
+  return RUNLORA_OK;
+}
+
+// ------------------------------------------------------------ selector
+void fill_flops(const runlora_shape_t* s, runlora_plan_t* p) {
+  for (int v = 1; v <= 2; ++v) flops_of(s, 0, v, &p->flops_fwd[v]);
+  for (int v = 1; v <= 8; ++v) flops_of(s, 1, v, &p->flops_bwd[v]);
+  int bf = 1, bb = 1;
+  for (int v = 2; v <= 2; ++v)
+    if (p->flops_fwd[v] < p->flops_fwd[bf]) bf = v;
+  for (int v = 2; v <= 5; ++v)
+    if (p->flops_bwd[v] < p->flops_bwd[bb]) bb = v;  // strict: ties keep the lowest index
+  p->flops_fwd_pick = bf;
+  p->flops_bwd_pick = bb;
+  p->param_reduction = (s->r * (s->k + s->m) < s->k * s->m) ? 1 : 0;
+}
+
+float median(std::vector<float> v) {
+  std::sort(v.begin(), v.end());
+  const size_t n = v.size();
+  return n % 2 ? v[n / 2] : 0.5f * (v[n / 2 - 1] + v[n / 2]);
+}
+
+}  // namespace
+
+// ============================================================== exported ABI
+extern "C" {
+
+const char* runlora_version(void) { return "runlora-b200 0.1 (sm_100a, tcgen05/TMA)"; }
+
+runlora_status_t runlora_create(runlora_handle_t* out, int device) {
+  if (!out) return fail(RUNLORA_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  int major = 0, minor = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+  if (major != 10 || minor != 0) {
+    char b[128];
+    snprintf(b, sizeof b, "device %d is sm_%d%d; this library is built for sm_100a (B200) only", device, major, minor);
+    return fail(RUNLORA_ERR_DEVICE, b);
+  }
+  try {
+    runlora_handle_s* h = new runlora_handle_s;
+    h->ctx = new Ctx(device);
+    *out = h;
+  } catch (...) {
+    return fail(RUNLORA_ERR_INVALID_ARG, "allocation of handle failed");
+  }
+  return RUNLORA_OK;
+}
+
+runlora_status_t runlora_destroy(runlora_handle_t h) {
+  if (!h) return RUNLORA_OK;
+  delete h->ctx;
+  delete h;
+  return RUNLORA_OK;
+}
+
+runlora_status_t runlora_flops(const runlora_shape_t* s, int is_backward, int variant, uint64_t* out) {
+  if (!s || !out) return fail(RUNLORA_ERR_INVALID_ARG, "shape/out is NULL");
+  if (s->n <= 0 || s->k <= 0 || s->m <= 0 || s->r <= 0)
+    return fail(RUNLORA_ERR_INVALID_ARG, "n, k, m, r must all be >= 1");
+  return flops_of(s, is_backward, variant, out);
+}
+
+int runlora_param_reduction(const runlora_shape_t* s) {
+  if (!s) return 0;
+  typedef unsigned __int128 u;
+  return ((u)s->r * ((u)s->k + (u)s->m) < (u)s->k * (u)s->m) ? 1 : 0;
+}
+
+runlora_status_t runlora_workspace_size(const runlora_shape_t* s, int fwd, int bwd, size_t* bytes) {
+  RL_TRY(check_shape(s));
+  if (!bytes) return fail(RUNLORA_ERR_INVALID_ARG, "bytes is NULL");
+  if (fwd < 0 || fwd > 2) return fail(RUNLORA_ERR_INVALID_ARG, "fwd must be 0, 1 or 2");
+  if (bwd < 0 || bwd > 8) return fail(RUNLORA_ERR_INVALID_ARG, "bwd must be 0..5");
+  if (bwd >= 6) return fail(RUNLORA_ERR_UNSUPPORTED_VARIANT, "backward6..8 are cost-model only (P:96-98)");
+  *bytes = layout_of(*s).total;  // one layout serves every variant
+  return RUNLORA_OK;
+}
+
+runlora_status_t runlora_select(runlora_handle_t h, const runlora_shape_t* s, int criterion,
+                                const runlora_operands_t* ops, void* ws, size_t ws_bytes, void* stream,
+                                runlora_plan_t* out) {
+  RL_TRY(check_shape(s));
+  if (!out) return fail(RUNLORA_ERR_INVALID_ARG, "out is NULL");
+  if (criterion < RUNLORA_BY_FLOPS || criterion > RUNLORA_HYBRID)
+    return fail(RUNLORA_ERR_INVALID_ARG, "criterion must be BY_FLOPS, BY_TIME or HYBRID");
+  runlora_plan_t p;
+  memset(&p, 0, sizeof p);
+  for (int v = 0; v < 3; ++v) p.time_fwd_us[v] = NAN;
+  for (int v = 0; v < 9; ++v) p.time_bwd_us[v] = NAN;
+  p.criterion = criterion;
+  {
+    uint64_t tmp;
+    RL_TRY(flops_of(s, 1, 6, &tmp));  // overflow check of the largest rows
+    RL_TRY(flops_of(s, 1, 4, &tmp));
+  }
+  fill_flops(s, &p);
+  p.fwd = p.flops_fwd_pick;
+  p.bwd = p.flops_bwd_pick;
+  if (criterion == RUNLORA_BY_FLOPS) {
+    *out = p;
+    return RUNLORA_OK;
+  }
+  RL_TRY(check_handle(h));
+  std::vector<int64_t> key = {s->n, s->k, s->m, s->r, s->dtype, criterion, ops ? ops->grad_dtype : -1};
+  {
+    std::lock_guard<std::mutex> g(h->ctx->plan_mu);
+    auto it = h->ctx->plans.find(key);
+    if (it != h->ctx->plans.end()) {
+      *out = it->second;
+      return RUNLORA_OK;
+    }
+  }
+  if (!ops) return fail(RUNLORA_ERR_INVALID_ARG, "time-based selection needs device operands");
+  DeviceGuard dg(h->ctx->device());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaEvent_t e0, e1;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
+    return fail(RUNLORA_ERR_TIMING, "cudaEventCreate failed");
+  const int warm = 3, reps = 15;
+  auto time_it = [&](auto&& run, float* med) -> runlora_status_t {
+    std::vector<float> t;
+    for (int i = 0; i < warm + reps; ++i) {
+      cudaEventRecord(e0, st);
+      RL_TRY(run());
+      cudaEventRecord(e1, st);
+      if (cudaEventSynchronize(e1) != cudaSuccess) return fail(RUNLORA_ERR_TIMING, "event sync failed");
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (i >= warm) t.push_back(ms * 1000.f);
+    }
+    *med = median(t);
+    return RUNLORA_OK;
+  };
+  const uint64_t fmin = std::min(p.flops_fwd[1], p.flops_fwd[2]);
+  uint64_t bmin = p.flops_bwd[1];
+  for (int v = 2; v <= 5; ++v) bmin = std::min(bmin, p.flops_bwd[v]);
+  runlora_status_t st_all = RUNLORA_OK;
+  for (int v = 1; v <= 2 && st_all == RUNLORA_OK; ++v) {
+    if (criterion == RUNLORA_HYBRID && p.flops_fwd[v] > 2 * fmin) continue;
+    st_all = time_it([&] { return do_forward(h, v, s, ops->X, ops->W, ops->A, ops->B, ops->Y, ws, ws_bytes, stream); },
+                     &p.time_fwd_us[v]);
+  }
+  for (int v = 1; v <= 5 && st_all == RUNLORA_OK; ++v) {
+    if (criterion == RUNLORA_HYBRID && p.flops_bwd[v] > 2 * bmin) continue;
+    st_all = time_it(
+        [&] {
+          return do_backward(h, v, s, ops->X, ops->W, ops->A, ops->B, ops->dY, ops->dX, ops->dA, ops->dB,
+                             ops->grad_dtype, 0, ws, ws_bytes, stream);
+        },
+        &p.time_bwd_us[v]);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (st_all != RUNLORA_OK) return st_all;
+  int bf = 0, bb = 0;
+  for (int v = 1; v <= 2; ++v)
+    if (!std::isnan(p.time_fwd_us[v]) && (bf == 0 || p.time_fwd_us[v] < p.time_fwd_us[bf])) bf = v;
+  for (int v = 1; v <= 5; ++v)
+    if (!std::isnan(p.time_bwd_us[v]) && (bb == 0 || p.time_bwd_us[v] < p.time_bwd_us[bb])) bb = v;
+  if (bf == 0 || bb == 0) return fail(RUNLORA_ERR_TIMING, "no candidate could be timed");
+  p.fwd = bf;
+  p.bwd = bb;
+  {
+    std::lock_guard<std::mutex> g(h->ctx->plan_mu);
+    h->ctx->plans[key] = p;
+  }
+  *out = p;
+  return RUNLORA_OK;
+}
+
+runlora_status_t runlora_forward(runlora_handle_t h, int fwd, const runlora_shape_t* s, const void* X, const void* W,
+                                 const void* A, const void* B, void* Y, void* ws, size_t ws_bytes, void* stream) {
+  return do_forward(h, fwd, s, X, W, A, B, Y, ws, ws_bytes, stream);
+}
+
+runlora_status_t runlora_backward(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X, const void* W,
+                                  const void* A, const void* B, const void* dY, void* dX, void* dA, void* dB,
+                                  int grad_dtype, int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  return do_backward(h, bwd, s, X, W, A, B, dY, dX, dA, dB, grad_dtype, accumulate, ws, ws_bytes, stream);
+}
+
+runlora_status_t runlora_backward_params(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X,
+                                         const void* W, const void* A, const void* B, const void* dY, void* dA,
+                                         void* dB, int grad_dtype, int accumulate, void* ws, size_t ws_bytes,
+                                         void* stream) {
+  return do_params(h, bwd, s, X, W, A, B, dY, dA, dB, grad_dtype, accumulate, ws, ws_bytes, stream);
+}
+
+runlora_status_t runlora_backward_input(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X,
+                                        const void* W, const void* A, const void* B, const void* dY, void* dX,
+                                        void* ws, size_t ws_bytes, void* stream) {
+  (void)X;
+  return do_input(h, bwd, s, W, A, B, dY, dX, ws, ws_bytes, stream);
+}
+
+runlora_status_t runlora_step_host(runlora_handle_t h, const runlora_shape_t* s, const runlora_host_step_t* t,
+                                   void* ws, size_t ws_bytes, void* stream) {
+  RL_TRY(check_handle(h));
+  RL_TRY(check_shape(s));
+  if (!t) return fail(RUNLORA_ERR_INVALID_ARG, "step is NULL");
+  if (!t->X_host || !t->dY_host || !t->dA_host || !t->dB_host)
+    return fail(RUNLORA_ERR_INVALID_ARG, "X_host, dY_host, dA_host, dB_host must be non-NULL");
+  DeviceGuard dg(h->ctx->device());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t es = s->dtype == RUNLORA_BF16 ? 2 : 4;
+  const size_t ges = t->grad_dtype == RUNLORA_BF16 ? 2 : 4;
+  const size_t xb = (size_t)s->n * s->k * es, yb = (size_t)s->n * s->m * es;
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(t->X, t->X_host, xb, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return cuda_fail(e, "H2D X");
+  if ((e = cudaMemcpyAsync(t->dY, t->dY_host, yb, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return cuda_fail(e, "H2D dY");
+  RL_TRY(do_forward(h, t->fwd, s, t->X, t->W, t->A, t->B, t->Y, ws, ws_bytes, stream));
+  RL_TRY(do_backward(h, t->bwd, s, t->X, t->W, t->A, t->B, t->dY, t->dX, t->dA, t->dB, t->grad_dtype, t->accumulate,
+                     ws, ws_bytes, stream));
+  if ((e = cudaMemcpyAsync(t->dA_host, t->dA, (size_t)s->k * s->r * ges, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return cuda_fail(e, "D2H dA");
+  if ((e = cudaMemcpyAsync(t->dB_host, t->dB, (size_t)s->r * s->m * ges, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return cuda_fail(e, "D2H dB");
+  if (t->Y_host && (e = cudaMemcpyAsync(t->Y_host, t->Y, yb, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return cuda_fail(e, "D2H Y");
+  if (t->dX_host && t->dX && (e = cudaMemcpyAsync(t->dX_host, t->dX, xb, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return cuda_fail(e, "D2H dX");
+  return RUNLORA_OK;
+}
+
+runlora_status_t runlora_profile_enable(runlora_handle_t h, int enable) {
+  RL_TRY(check_handle(h));
+  h->ctx->profile_enable(enable != 0);
+  return RUNLORA_OK;
+}
+
+runlora_status_t runlora_profile_read(runlora_handle_t h, runlora_kernel_stat_t* stats, int max_stats, int* count,
+                                      int reset) {
+  RL_TRY(check_handle(h));
+  std::string err;
+  DeviceGuard dg(h->ctx->device());
+  if (!h->ctx->profile_read(stats, max_stats, count, reset != 0, &err)) return fail(RUNLORA_ERR_CUDA, err);
+  return RUNLORA_OK;
+}
+
+uint64_t runlora_launch_count(runlora_handle_t h) { return (h && h->ctx) ? h->ctx->launches() : 0; }
+
+const char* runlora_status_string(runlora_status_t st) {
+  switch (st) {
+    case RUNLORA_OK: return "ok";
+    case RUNLORA_ERR_INVALID_ARG: return "invalid argument";
+    case RUNLORA_ERR_SHAPE: return "shape mismatch";
+    case RUNLORA_ERR_DTYPE: return "unsupported dtype";
+    case RUNLORA_ERR_UNSUPPORTED_VARIANT: return "unsupported variant";
+    case RUNLORA_ERR_OVERFLOW: return "FLOP count overflow";
+    case RUNLORA_ERR_ALIGNMENT: return "alignment";
+    case RUNLORA_ERR_WORKSPACE: return "workspace too small";
+    case RUNLORA_ERR_CUDA: return "CUDA error";
+    case RUNLORA_ERR_TIMING: return "timing failure";
+    case RUNLORA_ERR_DEVICE: return "unsupported device";
+  }
+  return "unknown status";
+}
+
+const char* runlora_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"
+
+// ------------------------------------------------------------ test hook
+#include "../../include/runlora_testing.h"
+extern "C" runlora_status_t runlora_debug_gemm(runlora_handle_t h, int M, int N, int K1, const void* A1, int a_mn,
+                                               const void* B1, int b_mn, int K2, const void* A2, const void* B2,
+                                               int out_mode, void* D, const void* Cin, int BN, int splits,
+                                               void* stream) {
+  RL_TRY(check_handle(h));
+  if (M <= 0 || N <= 0 || K1 <= 0 || K2 < 0 || splits < 1) return fail(RUNLORA_ERR_INVALID_ARG, "bad gemm dims");
+  GemmReq q = base_req(M, N, KID_GEMM_MAIN);
+  q.a = a_mn ? mat(A1, K1, M) : mat(A1, M, K1);
+  q.a_mn = a_mn != 0;
+  q.b = b_mn ? mat(B1, K1, N) : mat(B1, N, K1);
+  q.b_mn = b_mn != 0;
+  q.K1 = K1;
+  if (K2 > 0) {
+    q.a2 = a_mn ? mat(A2, K2, M) : mat(A2, M, K2);
+    q.b2 = b_mn ? mat(B2, K2, N) : mat(B2, N, K2);
+    q.K2 = K2;
+  }
+  q.out_mode = out_mode;
+  q.D = D;
+  q.ldd = N;
+  q.Cin = Cin;
+  q.ldc = N;
+  q.BN = BN;
+  const int nk = (K1 + kBK - 1) / kBK;
+  q.splits = splits;
+  q.kb_per_split = (nk + splits - 1) / splits;
+  q.splits = (nk + q.kb_per_split - 1) / q.kb_per_split;
+  q.split_stride = (int64_t)M * N;
+  DeviceGuard dg(h->ctx->device());
+  RL_TRY(gemm(*h->ctx, q, static_cast<cudaStream_t>(stream)));
+  return post_launch();
+}

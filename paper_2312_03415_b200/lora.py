@@ -1,0 +1,62 @@
+"""Autograd integration: a LoRA linear whose forward/backward run through the
+C ABI with the plan chosen by the selector.
+
+Paper: "neither forward function in RunLoRA saves result of XA to context"
+— the context holds X (and references to the frozen W and the adapters A, B);
+the backward recomputes whatever bracketing it needs (Alg. 1-5).
+Layouts follow the paper: X[n,k], W[k,m], A[k,r], B[r,m] (Y = XW).
+"""
+from __future__ import annotations
+
+import torch
+
+from . import runlora as rl
+
+
+def _shape(X, W, A):
+    n, k = X.shape
+    m = W.shape[1]
+    r = A.shape[1]
+    return rl.make_shape(n, k, m, r, X.dtype)
+
+
+class LoRALinearFunction(torch.autograd.Function):
+    """Y = LoRA(X) with forward variant plan.fwd and backward variant plan.bwd."""
+
+    @staticmethod
+    def forward(ctx, X, W, A, B, fwd: int, bwd: int):
+        for t, name in ((X, "X"), (W, "W"), (A, "A"), (B, "B")):
+            if not t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous CUDA tensor")
+        shape = _shape(X, W, A)
+        h = rl.handle(X.device)
+        Y = torch.empty(X.shape[0], W.shape[1], dtype=X.dtype, device=X.device)
+        h.forward(fwd, shape, X, W, A, B, Y)
+        ctx.save_for_backward(X, W, A, B)   # no XA
+        ctx.bwd = bwd
+        ctx.need_dx = ctx.needs_input_grad[0]
+        return Y
+
+    @staticmethod
+    def backward(ctx, dY):
+        X, W, A, B = ctx.saved_tensors
+        dY = dY.contiguous()
+        shape = _shape(X, W, A)
+        h = rl.handle(X.device)
+        gdt = torch.float32 if X.dtype == torch.float32 else A.dtype
+        dA = torch.empty(A.shape, dtype=gdt, device=X.device)
+        dB = torch.empty(B.shape, dtype=gdt, device=X.device)
+        dX = torch.empty_like(X) if ctx.need_dx else None
+        h.backward(ctx.bwd, shape, X, W, A, B, dY, dX, dA, dB)
+        return dX, None, dA.to(A.dtype), dB.to(B.dtype), None, None
+
+
+def lora_linear(X, W, A, B, plan=None, criterion=rl.BY_FLOPS):
+    """Functional entry: selects the (forward, backward) pair for this shape (cached
+    per shape by the library for time-based criteria) and applies it."""
+    if plan is None:
+        shape = _shape(X, W, A)
+        plan = rl.select_by_flops(shape) if criterion == rl.BY_FLOPS else None
+        if plan is None:
+            raise ValueError("time-based selection needs operands: call Handle.select(..., ops=...) first")
+    return LoRALinearFunction.apply(X, W, A, B, int(plan.fwd), int(plan.bwd))
