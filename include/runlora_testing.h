@@ -12,7 +12,8 @@
  *   A2/B2: same majors with K2 (K2 == 0: no tail)
  *   out_mode 0: D bf16 [M, N]; 1: D bf16 = acc + Cin (bf16 [M, N]);
  *            2: D fp32 partial slabs [splits][M][N] (split-K over K1)
- *   BN: tile width (16, 32, 48, 64, 128, 256; MN-major B needs a multiple of 64).
+ *   BN: tile width (16, 32, 48, 64, 128, 256; MN-major B: 16, 32 or a multiple of 64).
+ *   cg: 1 = one CTA per 128-row tile; 2 = CTA pair (tcgen05 cta_group::2) per 256-row tile.
  * All pointers are device pointers; rows are contiguous (ld = number of columns).
  */
 #ifndef RUNLORA_TESTING_H_
@@ -23,7 +24,7 @@ extern "C" {
 #endif
 runlora_status_t runlora_debug_gemm(runlora_handle_t h, int M, int N, int K1, const void* A1, int a_mn,
                                     const void* B1, int b_mn, int K2, const void* A2, const void* B2, int out_mode,
-                                    void* D, const void* Cin, int BN, int splits, void* stream);
+                                    void* D, const void* Cin, int BN, int splits, int cg, void* stream);
 #ifdef __cplusplus
 }
 #endif

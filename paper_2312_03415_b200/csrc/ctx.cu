@@ -1,6 +1,7 @@
 // Per-handle host context: device facts, TMA descriptor cache, launch counting
 // and CUDA-event kernel profiling.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -19,6 +20,7 @@ Ctx::Ctx(int device) : device_(device) {
   if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
       q == cudaDriverEntryPointSuccess)
     encode_fn_ = fn;
+  if (const char* e = getenv("RUNLORA_MAIN_CG")) main_cg_ = atoi(e) == 1 ? 1 : 2;
 }
 
 Ctx::~Ctx() {
@@ -30,10 +32,10 @@ Ctx::~Ctx() {
   if (cur_start_) cudaEventDestroy(cur_start_);
 }
 
-bool Ctx::tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* err) {
+bool Ctx::tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* err, int swz, int chunks) {
   char key[160];
-  snprintf(key, sizeof key, "%p/%lld/%lld/%lld/%d", m.ptr, (long long)m.rows, (long long)m.cols, (long long)m.ld,
-           box_rows);
+  snprintf(key, sizeof key, "%p/%lld/%lld/%lld/%d/%d/%d", m.ptr, (long long)m.rows, (long long)m.cols,
+           (long long)m.ld, box_rows, swz, chunks);
   {
     std::lock_guard<std::mutex> g(tmap_mu_);
     auto it = tmaps_.find(key);
@@ -46,20 +48,30 @@ bool Ctx::tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* 
     if (err) *err = "cuTensorMapEncodeTiled entry point unavailable";
     return false;
   }
-  cuuint64_t dims[2] = {(cuuint64_t)m.cols, (cuuint64_t)m.rows};
-  cuuint64_t strides[1] = {(cuuint64_t)m.ld * 2};
-  cuuint32_t box[2] = {64u, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1u, 1u};
+  const cuuint32_t w = (cuuint32_t)(swz / 2);
+  cuuint64_t dims[3] = {(cuuint64_t)m.cols, (cuuint64_t)m.rows, 1};
+  cuuint64_t strides[2] = {(cuuint64_t)m.ld * 2, 0};
+  cuuint32_t box[3] = {w, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  cuuint32_t rank = 2;
+  if (chunks > 0) {
+    dims[0] = w;
+    dims[2] = (cuuint64_t)(m.cols / w);
+    strides[1] = (cuuint64_t)w * 2;
+    box[2] = (cuuint32_t)chunks;
+    rank = 3;
+  }
   CUtensorMap tm;
   CUresult r = reinterpret_cast<EncodeTiledFn>(encode_fn_)(
-      &tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(m.ptr), dims, strides, box, estr,
-      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      &tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(m.ptr), dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE,
+      swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     if (err) {
       char buf[256];
-      snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d) for %lldx%lld ld=%lld box=64x%d ptr=%p", (int)r,
-               (long long)m.rows, (long long)m.cols, (long long)m.ld, box_rows, m.ptr);
+      snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d) for %lldx%lld ld=%lld box=%dx%d ptr=%p", (int)r,
+               (long long)m.rows, (long long)m.cols, (long long)m.ld, swz / 2, box_rows, m.ptr);
       *err = buf;
     }
     return false;

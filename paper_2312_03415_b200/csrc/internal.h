@@ -52,6 +52,7 @@ struct GemmReq {
   int splits;        // >= 1 (only with OUT_F32)
   int kb_per_split;
   bool a_stream_once;  // A operand is read once (evict-first hint)
+  int cg;              // 1: one CTA per 128-row tile; 2: CTA pair (cta_group::2) per 256-row tile
   KernelId kid;
 };
 
@@ -61,10 +62,14 @@ class Ctx {
   ~Ctx();
   int device() const { return device_; }
   int num_sms() const { return num_sms_; }
+  int main_cg() const { return main_cg_; }  // CTA-group size of the Y / dX GEMMs (env RUNLORA_MAIN_CG)
 
-  // Encodes (or fetches from cache) a 2-D bf16 TMA descriptor with 128B swizzle:
-  // dims {cols, rows}, row stride ld*2 bytes, box {64, box_rows}.
-  bool tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* err);
+  // Encodes (or fetches from cache) a 2-D bf16 TMA descriptor with swz_bytes swizzle
+  // (32, 64, 128): dims {cols, rows}, row stride ld*2 bytes, box {swz_bytes/2, box_rows}.
+  // chunks > 0: 3-D view {swz/2, rows, cols/(swz/2)} (chunk stride swz bytes), box
+  // {swz/2, box_rows, chunks} -> one TMA op fills `chunks` adjacent swizzle columns.
+  bool tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* err, int swz_bytes = 128,
+            int chunks = 0);
 
   // Profiling hooks around every launch.
   void launch_begin(cudaStream_t s, KernelId kid);
@@ -79,6 +84,7 @@ class Ctx {
  private:
   int device_;
   int num_sms_ = 148;
+  int main_cg_ = 2;
   void* encode_fn_ = nullptr;
   std::mutex tmap_mu_;
   std::unordered_map<std::string, CUtensorMap> tmaps_;
@@ -98,10 +104,21 @@ class Ctx {
 };
 
 // Kernel launchers (kernels.cu). Return cudaSuccess or the launch error.
-cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq& r, cudaStream_t s, std::string* err);
-cudaError_t launch_splitk_reduce(Ctx& ctx, const float* P, int splits, int64_t split_stride, int rows, int cols,
-                                 int64_t ldp, void* out, bool out_bf16, int64_t ldo, bool transpose,
-                                 bool accumulate, cudaStream_t s);
+cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t s, std::string* err);
+// Fixed-order sum of fp32 split-K slabs P[split][rows][ldp] (first `cols` columns) into
+// out (fp32 or bf16; optionally transposed: out[j*ldo + i]; optionally accumulated).
+struct ReduceJob {
+  const float* P;
+  int splits;
+  int64_t split_stride;
+  int rows, cols;
+  int64_t ldp;
+  void* out;
+  int out_bf16;
+  int64_t ldo;
+  int transpose, accumulate;
+};
+cudaError_t launch_splitk_reduce(Ctx& ctx, const ReduceJob* jobs, int njobs, cudaStream_t s);
 // fp32 SIMT GEMM: C[i,j] = (acc ? C[i,j] : 0) + (Cadd ? Cadd[i,j] : 0) + sum_t A(i,t) B(t,j),
 // A(i,t) = A[i*sa0 + t*sa1], B(t,j) = B[t*sb0 + j*sb1].
 cudaError_t launch_sgemm(Ctx& ctx, int M, int N, int K, const float* A, int64_t sa0, int64_t sa1, const float* B,

@@ -2,6 +2,8 @@
 // fp32 SIMT GEMM.  See tc_gemm.cuh for the GEMM design.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+#include <cstring>
 #include <string>
 
 #include "internal.h"
@@ -18,65 +20,85 @@ namespace {
 
 constexpr int kMaxDevices = 64;
 
-template <int BN, bool AM, bool BM>
-cudaError_t run_tc(Ctx& ctx, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ta2,
-                   const CUtensorMap& tb2, const GemmArgs& g, int units, cudaStream_t s) {
-  auto kern = tc_gemm_kernel<BN, AM, BM>;
+template <int BN, int CG>
+cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, const GemmArgs& g, cudaStream_t s) {
+  auto kern = tc_gemm_kernel<BN, CG>;
+  constexpr uint32_t smem = TileCfg<BN, CG>::SMEM_BYTES;
   static bool attr_set[kMaxDevices] = {};
   const int dev = ctx.device();
   if (dev < kMaxDevices && !attr_set[dev]) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileCfg<BN>::SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
   }
-  const int grid = units < ctx.num_sms() ? units : ctx.num_sms();
-  kern<<<grid, kGemmThreads, TileCfg<BN>::SMEM_BYTES, s>>>(ta, tb, ta2, tb2, g);
-  return cudaGetLastError();
+  const int groups_max = ctx.num_sms() / CG;
+  const int groups = g.total_units < groups_max ? g.total_units : groups_max;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(groups * CG);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (CG > 1) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, tm, g);
 }
 
-template <bool AM, bool BM>
-cudaError_t dispatch_bn(Ctx& ctx, int BN, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ta2,
-                        const CUtensorMap& tb2, const GemmArgs& g, int units, cudaStream_t s) {
-  if constexpr (BM) {
-    switch (BN) {
-      case 64: return run_tc<64, AM, BM>(ctx, ta, tb, ta2, tb2, g, units, s);
-      case 128: return run_tc<128, AM, BM>(ctx, ta, tb, ta2, tb2, g, units, s);
-      case 256: return run_tc<256, AM, BM>(ctx, ta, tb, ta2, tb2, g, units, s);
-      default: return cudaErrorInvalidValue;
-    }
-  } else {
-    switch (BN) {
-      case 16: return run_tc<16, AM, BM>(ctx, ta, tb, ta2, tb2, g, units, s);
-      case 32: return run_tc<32, AM, BM>(ctx, ta, tb, ta2, tb2, g, units, s);
-      case 48: return run_tc<48, AM, BM>(ctx, ta, tb, ta2, tb2, g, units, s);
-      case 64: return run_tc<64, AM, BM>(ctx, ta, tb, ta2, tb2, g, units, s);
-      case 128: return run_tc<128, AM, BM>(ctx, ta, tb, ta2, tb2, g, units, s);
-      case 256: return run_tc<256, AM, BM>(ctx, ta, tb, ta2, tb2, g, units, s);
-      default: return cudaErrorInvalidValue;
-    }
+cudaError_t dispatch_tc(Ctx& ctx, int bn_max, int cg, const Tmaps& tm, const GemmArgs& g, cudaStream_t s) {
+  if (cg == 2) {
+    if (bn_max == 256) return run_tc<256, 2>(ctx, tm, g, s);
+    if (bn_max == 128) return run_tc<128, 2>(ctx, tm, g, s);
+    return cudaErrorInvalidValue;
+  }
+  switch (bn_max) {
+    case 16: return run_tc<16, 1>(ctx, tm, g, s);
+    case 32: return run_tc<32, 1>(ctx, tm, g, s);
+    case 48: return run_tc<48, 1>(ctx, tm, g, s);
+    case 64: return run_tc<64, 1>(ctx, tm, g, s);
+    case 128: return run_tc<128, 1>(ctx, tm, g, s);
+    case 256: return run_tc<256, 1>(ctx, tm, g, s);
+    default: return cudaErrorInvalidValue;
   }
 }
 
 // ------------------------------------------------------------ split-K reduce
-__global__ void splitk_reduce_kernel(const float* __restrict__ P, int splits, long long sstride, int rows, int cols,
-                                     long long ldp, void* __restrict__ out, int out_bf16, long long ldo,
-                                     int transpose, int accumulate) {
-  const long long total = (long long)rows * cols;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+struct ReduceArgs {
+  ReduceJob j[2];
+  long long total0, total;
+};
+
+__global__ void splitk_reduce_kernel(const __grid_constant__ ReduceArgs a) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < a.total;
        idx += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(idx / cols), j = (int)(idx % cols);
-    const float* p = P + (long long)i * ldp + j;
+    const bool second = idx >= a.total0;
+    const ReduceJob& J = a.j[second ? 1 : 0];
+    const long long e = second ? idx - a.total0 : idx;
+    // transposed outputs: walk the output row-major so that stores coalesce
+    int i, jj;
+    if (J.transpose) {
+      jj = (int)(e / J.rows);
+      i = (int)(e % J.rows);
+    } else {
+      i = (int)(e / J.cols);
+      jj = (int)(e % J.cols);
+    }
+    const float* p = J.P + (long long)i * J.ldp + jj;
     float acc = 0.f;
-    for (int sp = 0; sp < splits; ++sp) acc += p[sp * sstride];  // fixed order: deterministic
-    const long long o = transpose ? (long long)j * ldo + i : (long long)i * ldo + j;
-    if (out_bf16) {
-      __nv_bfloat16* d = static_cast<__nv_bfloat16*>(out) + o;
-      if (accumulate) acc += __bfloat162float(*d);
+    for (int sp = 0; sp < J.splits; ++sp) acc += p[sp * J.split_stride];  // fixed order: deterministic
+    const long long o = J.transpose ? (long long)jj * J.ldo + i : (long long)i * J.ldo + jj;
+    if (J.out_bf16) {
+      __nv_bfloat16* d = static_cast<__nv_bfloat16*>(J.out) + o;
+      if (J.accumulate) acc += __bfloat162float(*d);
       *d = __float2bfloat16_rn(acc);
     } else {
-      float* d = static_cast<float*>(out) + o;
-      if (accumulate) acc += *d;
+      float* d = static_cast<float*>(J.out) + o;
+      if (J.accumulate) acc += *d;
       *d = acc;
     }
   }
@@ -137,64 +159,99 @@ __global__ void __launch_bounds__(256) sgemm_kernel(int M, int N, int K, const f
 
 }  // namespace
 
-cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq& r, cudaStream_t s, std::string* err) {
-  CUtensorMap ta, tb, ta2, tb2;
-  const int a_box = r.a_mn ? 64 : kBM;
-  const int b_box = r.b_mn ? 64 : r.BN;
-  if (!ctx.tmap(r.a, a_box, &ta, err) || !ctx.tmap(r.b, b_box, &tb, err)) return cudaErrorInvalidValue;
-  if (r.K2 > 0) {
-    if (!ctx.tmap(r.a2, a_box, &ta2, err) || !ctx.tmap(r.b2, b_box, &tb2, err)) return cudaErrorInvalidValue;
-  } else {
-    ta2 = ta;
-    tb2 = tb;
+cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t s, std::string* err) {
+  if (nreq < 1 || nreq > 2) return cudaErrorInvalidValue;
+  Tmaps tm;
+  GemmArgs g;
+  memset(&g, 0, sizeof g);
+  const int cg = reqs[0].cg > 1 ? 2 : 1;
+  int bn_max = 0;
+  for (int q = 0; q < nreq; ++q) {
+    const GemmReq& r = reqs[q];
+    if ((r.cg > 1 ? 2 : 1) != cg) return cudaErrorInvalidValue;
+    // MN-major B: 128B swizzle in 64-column chunks, or one 16/32-column chunk (32B/64B swizzle)
+    const int nb = r.BN / cg;
+    const int b_swz = !r.b_mn ? 128 : (nb % 64 == 0 ? 128 : nb == 32 ? 64 : nb == 16 ? 32 : 0);
+    if (r.BN % (16 * cg) != 0 || b_swz == 0) {
+      if (err) *err = "tc_gemm: illegal tile width for operand majorness";
+      return cudaErrorInvalidValue;
+    }
+    const int a_box = r.a_mn ? 64 : kBM;
+    const int b_box = r.b_mn ? 64 : nb;
+    // MN-major operands whose contiguous extent is a whole number of swizzle chunks are
+    // fetched with ONE 3-D TMA box per stage instead of one 2-D box per chunk.
+    const int b_cw = b_swz / 2;
+    const bool a3 = r.a_mn && r.a.cols % 64 == 0 && (r.K2 == 0 || r.a2.cols % 64 == 0);
+    const bool b3 = r.b_mn && nb > b_cw && r.b.cols % b_cw == 0 && (r.K2 == 0 || r.b2.cols % b_cw == 0);
+    if (!ctx.tmap(r.a, a_box, &tm.m[q][0], err, 128, a3 ? 2 : 0) ||
+        !ctx.tmap(r.b, b_box, &tm.m[q][1], err, b_swz, b3 ? nb / b_cw : 0))
+      return cudaErrorInvalidValue;
+    if (r.K2 > 0) {
+      if (!ctx.tmap(r.a2, a_box, &tm.m[q][2], err, 128, a3 ? 2 : 0) ||
+          !ctx.tmap(r.b2, b_box, &tm.m[q][3], err, b_swz, b3 ? nb / b_cw : 0))
+        return cudaErrorInvalidValue;
+    } else {
+      tm.m[q][2] = tm.m[q][0];
+      tm.m[q][3] = tm.m[q][1];
+    }
+    Prob& p = g.p[q];
+    p.M = r.M;
+    p.N = r.N;
+    p.bn = r.BN;
+    p.k1 = r.K1;
+    p.nk1 = (r.K1 + kBK - 1) / kBK;
+    p.k2 = r.K2;
+    p.nk2 = r.K2 > 0 ? (r.K2 + kBK - 1) / kBK : 0;
+    p.num_splits = r.splits > 1 ? r.splits : 1;
+    p.kb_per_split = r.splits > 1 ? r.kb_per_split : p.nk1;
+    p.num_m_tiles = (r.M + kBM * cg - 1) / (kBM * cg);
+    p.num_n_tiles = (r.N + r.BN - 1) / r.BN;
+    p.units = p.num_m_tiles * p.num_n_tiles * p.num_splits;
+    p.a_mn = r.a_mn;
+    p.b_mn = r.b_mn;
+    p.b_swz = b_swz;
+    p.a_3d = a3 ? 1 : 0;
+    p.b_3d = b3 ? 1 : 0;
+    p.out_mode = r.out_mode;
+    p.idesc = idesc_bf16(kBM * cg, r.BN, r.a_mn, r.b_mn);
+    p.stage_tx = (uint32_t)cg * (uint32_t)(kBM * kBK * 2 + (r.BN / cg) * kBK * 2);
+    p.D = r.D;
+    p.ldd = r.ldd;
+    p.split_stride = r.split_stride;
+    p.Cin = static_cast<const __nv_bfloat16*>(r.Cin);
+    p.ldc = r.ldc;
+    p.hint_a = r.a_stream_once ? kEvictFirst : kEvictNormal;
+    p.hint_b = kEvictLast;
+    g.total_units += p.units;
+    if (r.BN > bn_max) bn_max = r.BN;
   }
-  GemmArgs g{};
-  g.M = r.M;
-  g.N = r.N;
-  g.k1 = r.K1;
-  g.nk1 = (r.K1 + kBK - 1) / kBK;
-  g.k2 = r.K2;
-  g.nk2 = r.K2 > 0 ? (r.K2 + kBK - 1) / kBK : 0;
-  g.kb_per_split = r.splits > 1 ? r.kb_per_split : g.nk1;
-  g.num_m_tiles = (r.M + kBM - 1) / kBM;
-  g.num_n_tiles = (r.N + r.BN - 1) / r.BN;
-  g.num_splits = r.splits > 1 ? r.splits : 1;
-  g.out_mode = r.out_mode;
-  g.D = r.D;
-  g.ldd = r.ldd;
-  g.split_stride = r.split_stride;
-  g.Cin = static_cast<const __nv_bfloat16*>(r.Cin);
-  g.ldc = r.ldc;
-  g.hint_a = r.a_stream_once ? kEvictFirst : kEvictNormal;
-  g.hint_b = kEvictLast;
-  const int units = g.num_m_tiles * g.num_n_tiles * g.num_splits;
-  if (units <= 0) return cudaSuccess;
-  ctx.launch_begin(s, r.kid);
-  cudaError_t e;
-  if (!r.a_mn && !r.b_mn)
-    e = dispatch_bn<false, false>(ctx, r.BN, ta, tb, ta2, tb2, g, units, s);
-  else if (!r.a_mn && r.b_mn)
-    e = dispatch_bn<false, true>(ctx, r.BN, ta, tb, ta2, tb2, g, units, s);
-  else if (r.a_mn && r.b_mn)
-    e = dispatch_bn<true, true>(ctx, r.BN, ta, tb, ta2, tb2, g, units, s);
-  else
-    e = cudaErrorNotSupported;  // MN-major A with K-major B is not used by any variant
+  g.nprob = nreq;
+  if (const char* d = getenv("RUNLORA_DBG_GEMM")) g.dbg = atoi(d);
+  if (nreq == 1) g.p[1] = g.p[0], g.p[1].units = 0;
+  if (g.total_units <= 0) return cudaSuccess;
+  ctx.launch_begin(s, reqs[0].kid);
+  cudaError_t e = dispatch_tc(ctx, bn_max, cg, tm, g, s);
   ctx.launch_end(s);
   if (e != cudaSuccess && err) *err = std::string("tc_gemm launch: ") + cudaGetErrorString(e);
   return e;
 }
 
-cudaError_t launch_splitk_reduce(Ctx& ctx, const float* P, int splits, int64_t split_stride, int rows, int cols,
-                                 int64_t ldp, void* out, bool out_bf16, int64_t ldo, bool transpose,
-                                 bool accumulate, cudaStream_t s) {
-  const long long total = (long long)rows * cols;
-  if (total <= 0) return cudaSuccess;
-  long long blocks = (total + 255) / 256;
+cudaError_t launch_splitk_reduce(Ctx& ctx, const ReduceJob* jobs, int njobs, cudaStream_t s) {
+  ReduceArgs a;
+  memset(&a, 0, sizeof a);
+  a.j[0] = jobs[0];
+  a.total0 = (long long)jobs[0].rows * jobs[0].cols;
+  a.total = a.total0;
+  if (njobs > 1) {
+    a.j[1] = jobs[1];
+    a.total += (long long)jobs[1].rows * jobs[1].cols;
+  }
+  if (a.total <= 0) return cudaSuccess;
+  long long blocks = (a.total + 255) / 256;
   const long long cap = (long long)ctx.num_sms() * 8;
   if (blocks > cap) blocks = cap;
   ctx.launch_begin(s, KID_SPLITK_REDUCE);
-  splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>(P, splits, split_stride, rows, cols, ldp, out, out_bf16 ? 1 : 0,
-                                                        ldo, transpose ? 1 : 0, accumulate ? 1 : 0);
+  splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>(a);
   ctx.launch_end(s);
   return cudaGetLastError();
 }

@@ -122,47 +122,182 @@ runlora_status_t flops_of(const runlora_shape_t* s, int is_backward, int v, uint
   return RUNLORA_OK;
 }
 
-// -------------------------------------------------------------- skinny plans
-constexpr int kSplitTargetUnits = 296;  // 2 x 148 SMs (fixed so workspace size is device-independent)
-constexpr int kMaxSplits = 16;
+size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+DeviceMat mat(const void* p, int64_t rows, int64_t cols) { return DeviceMat{p, rows, cols, cols}; }
 
-struct SkinnyPlan {
-  int BN, Npad, splits, kps;
+// -------------------------------------------------------------- skinny plans
+// A "skinny" product has a rank-r output axis: out[rows, r] = A_op[rows, K]·B_op[K, r].
+// One launch runs up to two of them (e.g. Z1 and Z2 together).  With enough row tiles
+// to fill the GPU they write bf16 directly; otherwise they split K (the long axis)
+// into fp32 partial slabs reduced in fixed order by one reducer launch (deterministic).
+constexpr int kSmTarget = 148;  // fixed so that workspace sizes are device-independent
+constexpr int kMaxSplits = 32;
+
+struct Skinny {
+  DeviceMat a;
+  bool a_mn;
+  DeviceMat b;
+  bool b_mn;
+  int64_t rows, K, r;
+  void* out;
+  bool out_bf16;
+  int64_t ldo;
+  bool transpose, accumulate;
 };
 
-int round_bn_k(int64_t r) {  // K-major B: smallest legal UMMA N >= r (<= 256)
+int skinny_bn(int64_t r, bool b_mn) {
+  if (b_mn) return r <= 16 ? 16 : r <= 32 ? 32 : r <= 64 ? 64 : r <= 128 ? 128 : 256;
   static const int opts[] = {16, 32, 48, 64, 128, 256};
   for (int o : opts)
     if (r <= o) return o;
   return 256;
 }
 
-SkinnyPlan plan_skinny(int64_t rows, int64_t K, int64_t r, bool b_mn) {
-  SkinnyPlan p;
-  p.BN = b_mn ? (r <= 64 ? 64 : r <= 128 ? 128 : 256) : round_bn_k(r);
-  const int64_t ntn = (r + p.BN - 1) / p.BN;
-  p.Npad = (int)(ntn * p.BN);
-  const int64_t tiles = ((rows + kBM - 1) / kBM) * ntn;
-  const int64_t kblocks = (K + kBK - 1) / kBK;
-  int64_t s = (kSplitTargetUnits + tiles - 1) / tiles;
-  s = std::min<int64_t>(s, kMaxSplits);
-  s = std::min<int64_t>(s, std::max<int64_t>(1, kblocks / 2));
-  s = std::max<int64_t>(s, 1);
-  p.kps = (int)((kblocks + s - 1) / s);
-  p.splits = (int)((kblocks + p.kps - 1) / p.kps);
+struct SkinnyPlan {
+  int n;             // jobs
+  bool direct;       // outputs written by the GEMM epilogue (no partials)
+  int BN[2], Npad[2], splits[2], kps[2];
+  size_t p_off[2];   // byte offsets of the partial slabs in the workspace P region
+  size_t p_bytes;    // total partial bytes
+};
+
+bool can_direct(const Skinny& j) { return j.out_bf16 && !j.transpose && !j.accumulate && j.ldo == j.r; }
+
+SkinnyPlan plan_skinny(const Skinny* jobs, int n) {
+  SkinnyPlan p{};
+  p.n = n;
+  int64_t tiles = 0, kb_max = 0;
+  bool direct_ok = true;
+  for (int i = 0; i < n; ++i) {
+    p.BN[i] = skinny_bn(jobs[i].r, jobs[i].b_mn);
+    const int64_t ntn = (jobs[i].r + p.BN[i] - 1) / p.BN[i];
+    p.Npad[i] = (int)(ntn * p.BN[i]);
+    tiles += ((jobs[i].rows + kBM - 1) / kBM) * ntn;
+    kb_max = std::max<int64_t>(kb_max, (jobs[i].K + kBK - 1) / kBK);
+    direct_ok = direct_ok && can_direct(jobs[i]);
+  }
+  // enough row tiles (>= 2/3 of the SMs busy) -> no split, direct bf16 epilogue
+  p.direct = direct_ok && 3 * tiles >= 2 * kSmTarget;
+  int64_t s = 1;
+  if (!p.direct) {
+    // choose the split count minimising (waves x k-blocks per unit) + a partial-traffic term
+    double best = 1e30;
+    for (int64_t c = 1; c <= kMaxSplits && c <= kb_max; ++c) {
+      const int64_t units = tiles * c;
+      const int64_t waves = (units + kSmTarget - 1) / kSmTarget;
+      const double cost = (double)waves * (double)((kb_max + c - 1) / c) + 0.25 * (double)c;
+      if (cost < best - 1e-9) {
+        best = cost;
+        s = c;
+      }
+    }
+  }
+  size_t off = 0;
+  for (int i = 0; i < n; ++i) {
+    const int64_t kb = (jobs[i].K + kBK - 1) / kBK;
+    const int64_t si = std::min<int64_t>(s, kb);
+    p.kps[i] = (int)((kb + si - 1) / si);
+    p.splits[i] = (int)((kb + p.kps[i] - 1) / p.kps[i]);
+    p.p_off[i] = off;
+    if (!p.direct) off += al((size_t)p.splits[i] * (size_t)jobs[i].rows * (size_t)p.Npad[i] * 4);
+  }
+  p.p_bytes = off;
   return p;
 }
 
-size_t partial_bytes(int64_t rows, int64_t K, int64_t r, bool b_mn) {
-  SkinnyPlan p = plan_skinny(rows, K, r, b_mn);
-  return (size_t)p.splits * (size_t)rows * (size_t)p.Npad * 4;
+GemmReq base_req(int M, int N, KernelId kid) {
+  GemmReq q;
+  memset(&q, 0, sizeof q);
+  q.M = M;
+  q.N = N;
+  q.splits = 1;
+  q.cg = 1;
+  q.kid = kid;
+  return q;
+}
+
+runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, KernelId kid, cudaStream_t st) {
+  const SkinnyPlan p = plan_skinny(jobs, n);
+  GemmReq q[2];
+  ReduceJob rj[2];
+  for (int i = 0; i < n; ++i) {
+    const Skinny& j = jobs[i];
+    q[i] = base_req((int)j.rows, p.direct ? (int)j.r : p.Npad[i], kid);
+    q[i].a = j.a;
+    q[i].a_mn = j.a_mn;
+    q[i].b = j.b;
+    q[i].b_mn = j.b_mn;
+    q[i].K1 = (int)j.K;
+    q[i].BN = p.BN[i];
+    q[i].a_stream_once = true;
+    float* Pi = reinterpret_cast<float*>(reinterpret_cast<char*>(P) + p.p_off[i]);
+    if (p.direct) {
+      q[i].out_mode = OUT_BF16;
+      q[i].D = j.out;
+      q[i].ldd = j.ldo;
+    } else {
+      q[i].out_mode = OUT_F32;
+      q[i].D = Pi;
+      q[i].ldd = p.Npad[i];
+      q[i].split_stride = j.rows * (int64_t)p.Npad[i];
+      q[i].splits = p.splits[i];
+      q[i].kb_per_split = p.kps[i];
+    }
+    rj[i] = ReduceJob{Pi, p.splits[i], j.rows * (int64_t)p.Npad[i], (int)j.rows, (int)j.r, p.Npad[i], j.out,
+                      j.out_bf16 ? 1 : 0, j.ldo, j.transpose ? 1 : 0, j.accumulate ? 1 : 0};
+  }
+  std::string err;
+  cudaError_t e = launch_tc_gemm(c, q, n, st, &err);
+  if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
+  if (!p.direct) {
+    e = launch_splitk_reduce(c, rj, n, st);
+    if (e != cudaSuccess) return cuda_fail(e, "splitk_reduce launch");
+  }
+  return RUNLORA_OK;
+}
+
+// Job builders (names follow Alg. 1-5).
+Skinny job_Z1(const runlora_shape_t& s, const void* dY, const void* B, void* z1) {  // Z1 = dY·Bᵀ
+  return Skinny{mat(dY, s.n, s.m), false, mat(B, s.r, s.m), false, s.n, s.m, s.r, z1, true, s.r, false, false};
+}
+Skinny job_Z2(const runlora_shape_t& s, const void* X, const void* A, void* z2) {  // Z2 = X·A
+  return Skinny{mat(X, s.n, s.k), false, mat(A, s.k, s.r), true, s.n, s.k, s.r, z2, true, s.r, false, false};
+}
+Skinny job_dA_tok(const runlora_shape_t& s, const void* X, const void* z1, void* dA, bool gb, bool acc) {
+  return Skinny{mat(X, s.n, s.k), true, mat(z1, s.n, s.r), true, s.k, s.n, s.r, dA, gb, s.r, false, acc};
+}
+Skinny job_dB_tok(const runlora_shape_t& s, const void* dY, const void* z2, void* dB, bool gb, bool acc) {
+  return Skinny{mat(dY, s.n, s.m), true, mat(z2, s.n, s.r), true, s.m, s.n, s.r, dB, gb, s.m, true, acc};
+}
+Skinny job_dA_dense(const runlora_shape_t& s, const void* z2d, const void* B, void* dA, bool gb, bool acc) {
+  return Skinny{mat(z2d, s.k, s.m), false, mat(B, s.r, s.m), false, s.k, s.m, s.r, dA, gb, s.r, false, acc};
+}
+Skinny job_dB_dense(const runlora_shape_t& s, const void* z2d, const void* A, void* dB, bool gb, bool acc) {
+  return Skinny{mat(z2d, s.k, s.m), true, mat(A, s.k, s.r), true, s.m, s.k, s.r, dB, gb, s.m, true, acc};
+}
+
+size_t partial_need(const runlora_shape_t& s) {
+  // every skinny launch group any variant issues; the P region covers the largest
+  const void* d = reinterpret_cast<const void*>(256);
+  void* o = reinterpret_cast<void*>(256);
+  Skinny g[8][2] = {
+      {job_Z2(s, d, d, o), job_Z2(s, d, d, o)},            // forward1: Z2 alone (slot 1 unused)
+      {job_Z1(s, d, d, o), job_Z2(s, d, d, o)},            // B1/B5 projections
+      {job_dA_tok(s, d, d, o, true, false), job_dB_tok(s, d, d, o, true, false)},
+      {job_Z1(s, d, d, o), job_Z1(s, d, d, o)},            // B2/B3 projection alone
+      {job_dA_tok(s, d, d, o, true, false), job_dB_dense(s, d, d, o, true, false)},
+      {job_dA_dense(s, d, d, o, true, false), job_dB_dense(s, d, d, o, true, false)},
+  };
+  const int counts[8] = {1, 2, 2, 1, 2, 2, 0, 0};
+  size_t need = 0;
+  for (int i = 0; i < 6; ++i) need = std::max(need, plan_skinny(g[i], counts[i]).p_bytes);
+  return need;
 }
 
 // ------------------------------------------------------------ workspace layout
 struct Layout {
   size_t z1, z2, wp, p, total;
 };
-size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 Layout layout_of(const runlora_shape_t& s) {
   const size_t es = s.dtype == RUNLORA_BF16 ? 2 : 4;
@@ -172,16 +307,7 @@ Layout layout_of(const runlora_shape_t& s) {
   L.z2 = al((size_t)n * r * es);
   L.wp = L.z2 + al((size_t)n * r * es);
   L.p = L.wp + al((size_t)k * m * es);
-  size_t pb = 0;
-  if (s.dtype == RUNLORA_BF16) {
-    pb = std::max(pb, partial_bytes(n, k, r, true));    // Z2 = X·A
-    pb = std::max(pb, partial_bytes(n, m, r, false));   // Z1 = dY·Bᵀ
-    pb = std::max(pb, partial_bytes(k, n, r, true));    // dA = Xᵀ·Z1
-    pb = std::max(pb, partial_bytes(m, n, r, true));    // dBᵀ = dYᵀ·Z2
-    pb = std::max(pb, partial_bytes(k, m, r, false));   // dA = Z2'·Bᵀ
-    pb = std::max(pb, partial_bytes(m, k, r, true));    // dBᵀ = Z2'ᵀ·A
-  }
-  L.total = L.p + al(pb);
+  L.total = L.p + (s.dtype == RUNLORA_BF16 ? partial_need(s) : 0);
   return L;
 }
 
@@ -207,49 +333,10 @@ runlora_status_t bind_ws(const runlora_shape_t& s, void* ws, size_t ws_bytes, Bu
   return RUNLORA_OK;
 }
 
-DeviceMat mat(const void* p, int64_t rows, int64_t cols) { return DeviceMat{p, rows, cols, cols}; }
-
 runlora_status_t gemm(Ctx& c, const GemmReq& q, cudaStream_t st) {
   std::string err;
-  cudaError_t e = launch_tc_gemm(c, q, st, &err);
+  cudaError_t e = launch_tc_gemm(c, &q, 1, st, &err);
   if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
-  return RUNLORA_OK;
-}
-
-GemmReq base_req(int M, int N, KernelId kid) {
-  GemmReq q;
-  memset(&q, 0, sizeof q);
-  q.M = M;
-  q.N = N;
-  q.splits = 1;
-  q.kid = kid;
-  return q;
-}
-
-// out = A_op[rows, K]·B_op[K, r]: fp32 split-K partials, then a fixed-order reduce
-// that casts (and optionally transposes / accumulates) into `out`.
-runlora_status_t skinny(Ctx& c, DeviceMat a, bool a_mn, DeviceMat b, bool b_mn, int64_t rows, int64_t K, int64_t r,
-                        void* out, bool out_bf16, int64_t ldo, bool transpose, bool accumulate, float* P,
-                        KernelId kid, cudaStream_t st) {
-  SkinnyPlan p = plan_skinny(rows, K, r, b_mn);
-  GemmReq q = base_req((int)rows, p.Npad, kid);
-  q.a = a;
-  q.a_mn = a_mn;
-  q.b = b;
-  q.b_mn = b_mn;
-  q.K1 = (int)K;
-  q.out_mode = OUT_F32;
-  q.D = P;
-  q.ldd = p.Npad;
-  q.split_stride = rows * (int64_t)p.Npad;
-  q.BN = p.BN;
-  q.splits = p.splits;
-  q.kb_per_split = p.kps;
-  q.a_stream_once = true;
-  RL_TRY(gemm(c, q, st));
-  cudaError_t e = launch_splitk_reduce(c, P, p.splits, q.split_stride, (int)rows, (int)r, p.Npad, out, out_bf16, ldo,
-                                       transpose, accumulate, st);
-  if (e != cudaSuccess) return cuda_fail(e, "splitk_reduce launch");
   return RUNLORA_OK;
 }
 
@@ -271,23 +358,30 @@ runlora_status_t wprime_bf16(Ctx& c, const runlora_shape_t& s, const void* W, co
   return gemm(c, q, st);
 }
 
+// The dominant Y / dX GEMMs: 256x256 tiles on CTA pairs (cta_group::2) unless disabled.
+GemmReq main_req(Ctx& c, int M, int N) {
+  GemmReq q = base_req(M, N, KID_GEMM_MAIN);
+  q.BN = 256;
+  q.cg = c.main_cg();
+  q.out_mode = OUT_BF16;
+  return q;
+}
+
 // ------------------------------------------------------------ bf16 variants
 runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* X, const void* W, const void* A,
                               const void* B, void* Y, Bufs& b, cudaStream_t st) {
   const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
-  GemmReq q = base_req((int)n, (int)m, KID_GEMM_MAIN);
+  GemmReq q = main_req(c, (int)n, (int)m);
   q.a = mat(X, n, k);
   q.a_mn = false;
   q.K1 = (int)k;
   q.b_mn = true;
-  q.out_mode = OUT_BF16;
   q.D = Y;
   q.ldd = m;
-  q.BN = 256;
   if (v == 1) {
-    // Z2 = X·A (never saved for the backward)
-    RL_TRY(skinny(c, mat(X, n, k), false, mat(A, k, r), true, n, k, r, b.z2, true, r, false, false, b.P,
-                  KID_GEMM_PROJ, st));
+    // Z2 = X·A (never saved for the backward), then Y = [X | Z2]·[W ; B]
+    Skinny j = job_Z2(s, X, A, b.z2);
+    RL_TRY(run_skinny(c, &j, 1, b.P, KID_GEMM_PROJ, st));
     q.b = mat(W, k, m);
     q.a2 = mat(b.z2, n, r);
     q.b2 = mat(B, r, m);
@@ -300,18 +394,19 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
 }
 
 runlora_status_t params_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* X, const void* A, const void* B,
-                             const void* dY, void* dA, void* dB, bool g_bf16, bool acc, Bufs& b, cudaStream_t st) {
-  const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
-  const bool need_z1 = v == 1 || v == 2 || v == 3 || v == 5;
-  const bool need_z2 = v == 1 || v == 5;
-  const bool dense = v == 2 || v == 3 || v == 4;
-  if (need_z1)  // Z1 = dY·Bᵀ: B_op[K=m, N=r] = Bᵀ, stored [N, K] = B -> K-major
-    RL_TRY(skinny(c, mat(dY, n, m), false, mat(B, r, m), false, n, m, r, b.z1, true, r, false, false, b.P,
-                  KID_GEMM_PROJ, st));
-  if (need_z2)  // Z2 = X·A
-    RL_TRY(skinny(c, mat(X, n, k), false, mat(A, k, r), true, n, k, r, b.z2, true, r, false, false, b.P,
-                  KID_GEMM_PROJ, st));
-  if (dense) {  // Z2' = Xᵀ·dY (k×m): A_op = Xᵀ (MN-major X), B_op = dY (MN-major)
+                             const void* dY, void* dA, void* dB, bool gb, bool acc, Bufs& b, cudaStream_t st) {
+  const int64_t n = s.n, k = s.k, m = s.m;
+  if (v == 1 || v == 5) {  // Alg. 1 / Alg. 5: Z1, Z2 | dA = Xᵀ·Z1, dB = Z2ᵀ·dY
+    Skinny pj[2] = {job_Z1(s, dY, B, b.z1), job_Z2(s, X, A, b.z2)};
+    RL_TRY(run_skinny(c, pj, 2, b.P, KID_GEMM_PROJ, st));
+    Skinny tj[2] = {job_dA_tok(s, X, b.z1, dA, gb, acc), job_dB_tok(s, dY, b.z2, dB, gb, acc)};
+    return run_skinny(c, tj, 2, b.P, KID_GEMM_TOKRED, st);
+  }
+  if (v == 2 || v == 3) {  // Z1 = dY·Bᵀ
+    Skinny j = job_Z1(s, dY, B, b.z1);
+    RL_TRY(run_skinny(c, &j, 1, b.P, KID_GEMM_PROJ, st));
+  }
+  {  // Z2' = Xᵀ·dY (k×m): A_op = Xᵀ (MN-major X), B_op = dY (MN-major)
     GemmReq q = base_req((int)k, (int)m, KID_GEMM_DENSE_XTDY);
     q.a = mat(X, n, k);
     q.a_mn = true;
@@ -322,37 +417,28 @@ runlora_status_t params_bf16(Ctx& c, int v, const runlora_shape_t& s, const void
     q.D = b.wp;
     q.ldd = m;
     q.BN = 256;
+    q.cg = c.main_cg();
     RL_TRY(gemm(c, q, st));
   }
-  // dA
-  if (v == 1 || v == 2 || v == 5)  // dA = Xᵀ·Z1 (token reduction, K = n)
-    RL_TRY(skinny(c, mat(X, n, k), true, mat(b.z1, n, r), true, k, n, r, dA, g_bf16, r, false, acc, b.P,
-                  KID_GEMM_TOKRED, st));
-  else  // dA = Z2'·Bᵀ
-    RL_TRY(skinny(c, mat(b.wp, k, m), false, mat(B, r, m), false, k, m, r, dA, g_bf16, r, false, acc, b.P,
-                  KID_GEMM_SMALL, st));
-  // dB (as dBᵀ[m, r], transposed by the reducer into dB[r, m])
-  if (v == 1 || v == 5)  // dBᵀ = dYᵀ·Z2
-    RL_TRY(skinny(c, mat(dY, n, m), true, mat(b.z2, n, r), true, m, n, r, dB, g_bf16, m, true, acc, b.P,
-                  KID_GEMM_TOKRED, st));
-  else  // dBᵀ = Z2'ᵀ·A
-    RL_TRY(skinny(c, mat(b.wp, k, m), true, mat(A, k, r), true, m, k, r, dB, g_bf16, m, true, acc, b.P,
-                  KID_GEMM_SMALL, st));
-  return RUNLORA_OK;
+  if (v == 2) {  // dA = Xᵀ·Z1, dB = Aᵀ·Z2'
+    Skinny j[2] = {job_dA_tok(s, X, b.z1, dA, gb, acc), job_dB_dense(s, b.wp, A, dB, gb, acc)};
+    return run_skinny(c, j, 2, b.P, KID_GEMM_SMALL, st);
+  }
+  // v = 3, 4: dA = Z2'·Bᵀ, dB = Aᵀ·Z2'
+  Skinny j[2] = {job_dA_dense(s, b.wp, B, dA, gb, acc), job_dB_dense(s, b.wp, A, dB, gb, acc)};
+  return run_skinny(c, j, 2, b.P, KID_GEMM_SMALL, st);
 }
 
 runlora_status_t input_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* W, const void* A, const void* B,
                             const void* dY, void* dX, Bufs& b, cudaStream_t st) {
   const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
-  GemmReq q = base_req((int)n, (int)k, KID_GEMM_MAIN);
+  GemmReq q = main_req(c, (int)n, (int)k);
   q.a = mat(dY, n, m);
   q.a_mn = false;
   q.b_mn = false;
   q.K1 = (int)m;
-  q.out_mode = OUT_BF16;
   q.D = dX;
   q.ldd = k;
-  q.BN = 256;
   if (v <= 3) {  // dX = [dY | Z1]·[Wᵀ ; Aᵀ]
     q.b = mat(W, k, m);  // B_op[K=m, N=k] = Wᵀ stored [N, K] = W: K-major
     q.a2 = mat(b.z1, n, r);
@@ -776,11 +862,12 @@ const char* runlora_last_error(void) { return g_last_error.c_str(); }
 #include "../../include/runlora_testing.h"
 extern "C" runlora_status_t runlora_debug_gemm(runlora_handle_t h, int M, int N, int K1, const void* A1, int a_mn,
                                                const void* B1, int b_mn, int K2, const void* A2, const void* B2,
-                                               int out_mode, void* D, const void* Cin, int BN, int splits,
+                                               int out_mode, void* D, const void* Cin, int BN, int splits, int cg,
                                                void* stream) {
   RL_TRY(check_handle(h));
   if (M <= 0 || N <= 0 || K1 <= 0 || K2 < 0 || splits < 1) return fail(RUNLORA_ERR_INVALID_ARG, "bad gemm dims");
   GemmReq q = base_req(M, N, KID_GEMM_MAIN);
+  q.cg = cg == 2 ? 2 : 1;
   q.a = a_mn ? mat(A1, K1, M) : mat(A1, M, K1);
   q.a_mn = a_mn != 0;
   q.b = b_mn ? mat(B1, K1, N) : mat(B1, N, K1);
@@ -798,7 +885,6 @@ extern "C" runlora_status_t runlora_debug_gemm(runlora_handle_t h, int M, int N,
   q.ldc = N;
   q.BN = BN;
   const int nk = (K1 + kBK - 1) / kBK;
-  q.splits = splits;
   q.kb_per_split = (nk + splits - 1) / splits;
   q.splits = (nk + q.kb_per_split - 1) / q.kb_per_split;
   q.split_stride = (int64_t)M * N;

@@ -19,11 +19,11 @@ def rl():
     f = runlora._lib.runlora_debug_gemm
     P, I = C.c_void_p, C.c_int
     f.restype = I
-    f.argtypes = [P, I, I, I, P, I, P, I, I, P, P, I, P, P, I, I, P]
+    f.argtypes = [P, I, I, I, P, I, P, I, I, P, P, I, P, P, I, I, I, P]
     return runlora
 
 
-def _run(rl, M, N, K1, a_mn, b_mn, BN, K2=0, out_mode=0, splits=1, seed=0):
+def _run(rl, M, N, K1, a_mn, b_mn, BN, K2=0, out_mode=0, splits=1, seed=0, cg=1):
     g = torch.Generator().manual_seed(seed)
     dev = "cuda"
     bf = torch.bfloat16
@@ -53,7 +53,7 @@ def _run(rl, M, N, K1, a_mn, b_mn, BN, K2=0, out_mode=0, splits=1, seed=0):
     h = rl.handle(0)
     st = rl._lib.runlora_debug_gemm(h._h, M, N, K1, a_st.data_ptr(), int(a_mn), b_st.data_ptr(), int(b_mn), K2,
                                     a2_st.data_ptr(), b2_st.data_ptr(), out_mode, D.data_ptr(), cin.data_ptr(), BN,
-                                    splits, C.c_void_p(torch.cuda.current_stream().cuda_stream))
+                                    splits, cg, C.c_void_p(torch.cuda.current_stream().cuda_stream))
     assert st == 0, rl._lib.runlora_last_error()
     torch.cuda.synchronize()
     got = D.double().cpu()
@@ -85,7 +85,34 @@ CASES = [
     (200, 264, 256, False, False, 256, 128),
     (200, 264, 256, False, True, 256, 72),
     (384, 512, 8, False, True, 256, 0),
+    # narrow MN-major B (32B / 64B swizzle)
+    (300, 16, 520, False, True, 16, 0),
+    (300, 8, 520, False, True, 16, 0),
+    (300, 32, 520, False, True, 32, 0),
+    (296, 24, 700, True, True, 32, 0),
+    (296, 16, 1000, True, True, 16, 0),
 ]
+
+CASES_CG2 = [
+    (256, 256, 64, False, False, 256, 0),
+    (256, 256, 64, False, True, 256, 0),
+    (520, 776, 328, False, False, 256, 0),
+    (520, 776, 328, False, True, 256, 0),
+    (300, 520, 256, False, True, 256, 16),
+    (300, 520, 256, False, False, 256, 16),
+    (300, 264, 256, False, False, 256, 136),
+    (512, 512, 1024, True, True, 256, 0),
+    (264, 384, 200, True, True, 256, 0),
+    (300, 256, 200, False, False, 128, 0),
+    (300, 256, 200, False, True, 128, 0),
+]
+
+
+@pytest.mark.parametrize("case", CASES_CG2)
+def test_gemm_cta_pair(rl, case):
+    M, N, K1, a_mn, b_mn, BN, K2 = case
+    err, _, _ = _run(rl, M, N, K1, a_mn, b_mn, BN, K2, cg=2)
+    assert err < 8e-3, err
 
 
 @pytest.mark.parametrize("case", CASES)
