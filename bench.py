@@ -170,6 +170,7 @@ def main():
     ap.add_argument("--impl", default="runlora", choices=["runlora", "reference"])
     ap.add_argument("--criterion", default="time", choices=["flops", "time", "hybrid"])
     ap.add_argument("--ref-tokens", type=int, default=512)
+    ap.add_argument("--plan", default=None, help="force a variant pair, e.g. 1,1 (skips selection)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-default-chain", action="store_true")
     args = ap.parse_args()
@@ -200,9 +201,14 @@ def main():
     dX = torch.empty(n, k, dtype=torch.bfloat16, device=dev)
     g = dp.PackedAdapterGrads.create(k, r, m, dev)
     crit = {"flops": rl.BY_FLOPS, "time": rl.BY_TIME, "hybrid": rl.HYBRID}[args.criterion]
+    if args.plan:
+        crit = rl.BY_FLOPS
+        args.criterion = "forced"
     plan = h.select(shape, crit, ops={"X": d["X"], "W": d["W"], "A": d["A"], "B": d["B"], "dY": d["dY"], "Y": Y,
                                       "dX": dX, "dA": g.dA, "dB": g.dB}, grad_dtype=rl.F32)
     fwd, bwd = plan.fwd, plan.bwd
+    if args.plan:
+        fwd, bwd = (int(x) for x in args.plan.split(","))
     if world > 1:
         fwd, bwd = dp.broadcast_plan(fwd, bwd, device=dev)
     comm = torch.cuda.Stream(dev) if world > 1 else None

@@ -21,6 +21,19 @@ Ctx::Ctx(int device) : device_(device) {
       q == cudaDriverEntryPointSuccess)
     encode_fn_ = fn;
   if (const char* e = getenv("RUNLORA_MAIN_CG")) main_cg_ = atoi(e) == 1 ? 1 : 2;
+  if (const char* e = getenv("RUNLORA_SPLITK_FIXUP")) fixup_ = atoi(e) != 0;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  if (cudaMalloc(&counters_, sizeof(int) * kCounterCap) == cudaSuccess) {
+    if (cudaMemset(counters_, 0, sizeof(int) * kCounterCap) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+      cudaFree(counters_);
+      counters_ = nullptr;
+    }
+  } else {
+    counters_ = nullptr;
+  }
+  if (prev >= 0) cudaSetDevice(prev);
 }
 
 Ctx::~Ctx() {
@@ -30,6 +43,23 @@ Ctx::~Ctx() {
   }
   for (auto e : free_events_) cudaEventDestroy(e);
   if (cur_start_) cudaEventDestroy(cur_start_);
+  if (counters_) cudaFree(counters_);
+  if (side_) cudaStreamDestroy(side_);
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
+}
+
+cudaStream_t Ctx::side_stream() {
+  if (!side_) cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking);
+  return side_;
+}
+cudaEvent_t Ctx::fork_event() {
+  if (!ev_fork_) cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming);
+  return ev_fork_;
+}
+cudaEvent_t Ctx::join_event() {
+  if (!ev_join_) cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming);
+  return ev_join_;
 }
 
 bool Ctx::tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* err, int swz, int chunks) {

@@ -54,6 +54,12 @@ struct GemmReq {
   bool a_stream_once;  // A operand is read once (evict-first hint)
   int cg;              // 1: one CTA per 128-row tile; 2: CTA pair (cta_group::2) per 256-row tile
   KernelId kid;
+  // in-kernel deterministic split-K fix-up (OUT_F32 + splits): see Prob in tc_gemm.cuh
+  int* counters;
+  int fix_cols;
+  void* fix_out;
+  int64_t fix_ldo;
+  int fix_bf16, fix_transpose, fix_accumulate;
 };
 
 class Ctx {
@@ -63,6 +69,15 @@ class Ctx {
   int device() const { return device_; }
   int num_sms() const { return num_sms_; }
   int main_cg() const { return main_cg_; }  // CTA-group size of the Y / dX GEMMs (env RUNLORA_MAIN_CG)
+  // Split-K tile counters (device, zero between launches; owned by the handle).
+  static constexpr int kCounterCap = 1 << 16;
+  int* counters() const { return counters_; }
+  bool fixup_enabled() const { return counters_ != nullptr && fixup_; }
+  // Side stream for small work that can overlap the next big GEMM (fork/join by events).
+  cudaStream_t side_stream();
+  cudaEvent_t fork_event();
+  cudaEvent_t join_event();
+  bool join_pending = false;
 
   // Encodes (or fetches from cache) a 2-D bf16 TMA descriptor with swz_bytes swizzle
   // (32, 64, 128): dims {cols, rows}, row stride ld*2 bytes, box {swz_bytes/2, box_rows}.
@@ -85,6 +100,10 @@ class Ctx {
   int device_;
   int num_sms_ = 148;
   int main_cg_ = 2;
+  int* counters_ = nullptr;
+  cudaStream_t side_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  bool fixup_ = false;  // env RUNLORA_SPLITK_FIXUP=1: in-kernel fix-up instead of the reducer launch
   void* encode_fn_ = nullptr;
   std::mutex tmap_mu_;
   std::unordered_map<std::string, CUtensorMap> tmaps_;

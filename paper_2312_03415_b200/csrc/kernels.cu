@@ -73,33 +73,51 @@ struct ReduceArgs {
   long long total0, total;
 };
 
-__global__ void splitk_reduce_kernel(const __grid_constant__ ReduceArgs a) {
+// One thread per (row i, 4-column group): float4 loads of every split slab in fixed
+// split order (deterministic), 4 slabs in flight at a time.  Column groups vary fastest
+// so a warp reads contiguous 512 B of each slab.
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constant__ ReduceArgs a) {
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < a.total;
        idx += (long long)gridDim.x * blockDim.x) {
     const bool second = idx >= a.total0;
     const ReduceJob& J = a.j[second ? 1 : 0];
     const long long e = second ? idx - a.total0 : idx;
-    // transposed outputs: walk the output row-major so that stores coalesce
-    int i, jj;
-    if (J.transpose) {
-      jj = (int)(e / J.rows);
-      i = (int)(e % J.rows);
-    } else {
-      i = (int)(e / J.cols);
-      jj = (int)(e % J.cols);
+    const int groups = (J.cols + 3) >> 2;
+    const int i = (int)(e / groups);
+    const int c0 = (int)(e % groups) * 4;
+    const float4* p = reinterpret_cast<const float4*>(J.P + (long long)i * J.ldp + c0);
+    const long long st4 = J.split_stride / 4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < J.splits; s0 += 16) {
+      float4 v[16];  // up to 16 slabs in flight, then summed in split order
+#pragma unroll
+      for (int x = 0; x < 16; ++x)
+        if (s0 + x < J.splits) v[x] = __ldg(p + (s0 + x) * st4);
+#pragma unroll
+      for (int x = 0; x < 16; ++x) {
+        if (s0 + x < J.splits) {
+          acc.x += v[x].x;
+          acc.y += v[x].y;
+          acc.z += v[x].z;
+          acc.w += v[x].w;
+        }
+      }
     }
-    const float* p = J.P + (long long)i * J.ldp + jj;
-    float acc = 0.f;
-    for (int sp = 0; sp < J.splits; ++sp) acc += p[sp * J.split_stride];  // fixed order: deterministic
-    const long long o = J.transpose ? (long long)jj * J.ldo + i : (long long)i * J.ldo + jj;
-    if (J.out_bf16) {
-      __nv_bfloat16* d = static_cast<__nv_bfloat16*>(J.out) + o;
-      if (J.accumulate) acc += __bfloat162float(*d);
-      *d = __float2bfloat16_rn(acc);
-    } else {
-      float* d = static_cast<float*>(J.out) + o;
-      if (J.accumulate) acc += *d;
-      *d = acc;
+    const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      if (c0 + x >= J.cols) break;
+      const long long o = J.transpose ? (long long)(c0 + x) * J.ldo + i : (long long)i * J.ldo + c0 + x;
+      float v = a4[x];
+      if (J.out_bf16) {
+        __nv_bfloat16* d = static_cast<__nv_bfloat16*>(J.out) + o;
+        if (J.accumulate) v += __bfloat162float(*d);
+        *d = __float2bfloat16_rn(v);
+      } else {
+        float* d = static_cast<float*>(J.out) + o;
+        if (J.accumulate) v += *d;
+        *d = v;
+      }
     }
   }
 }
@@ -220,6 +238,13 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
     p.split_stride = r.split_stride;
     p.Cin = static_cast<const __nv_bfloat16*>(r.Cin);
     p.ldc = r.ldc;
+    p.counters = r.counters;
+    p.fix_cols = r.fix_cols;
+    p.fix_out = r.fix_out;
+    p.fix_ldo = r.fix_ldo;
+    p.fix_bf16 = r.fix_bf16;
+    p.fix_transpose = r.fix_transpose;
+    p.fix_accumulate = r.fix_accumulate;
     p.hint_a = r.a_stream_once ? kEvictFirst : kEvictNormal;
     p.hint_b = kEvictLast;
     g.total_units += p.units;
@@ -240,15 +265,15 @@ cudaError_t launch_splitk_reduce(Ctx& ctx, const ReduceJob* jobs, int njobs, cud
   ReduceArgs a;
   memset(&a, 0, sizeof a);
   a.j[0] = jobs[0];
-  a.total0 = (long long)jobs[0].rows * jobs[0].cols;
+  a.total0 = (long long)jobs[0].rows * ((jobs[0].cols + 3) / 4);
   a.total = a.total0;
   if (njobs > 1) {
     a.j[1] = jobs[1];
-    a.total += (long long)jobs[1].rows * jobs[1].cols;
+    a.total += (long long)jobs[1].rows * ((jobs[1].cols + 3) / 4);
   }
   if (a.total <= 0) return cudaSuccess;
   long long blocks = (a.total + 255) / 256;
-  const long long cap = (long long)ctx.num_sms() * 8;
+  const long long cap = (long long)ctx.num_sms() * 16;
   if (blocks > cap) blocks = cap;
   ctx.launch_begin(s, KID_SPLITK_REDUCE);
   splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>(a);

@@ -216,10 +216,20 @@ GemmReq base_req(int M, int N, KernelId kid) {
   return q;
 }
 
-runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, KernelId kid, cudaStream_t st) {
+// defer_reduce: run the reducer on the handle's side stream (forked from `st` by an event)
+// so that it overlaps whatever the caller enqueues next on `st`; the caller must join
+// (cudaStreamWaitEvent(st, c.join_event())) before the outputs are consumed.
+runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, KernelId kid, cudaStream_t st,
+                            bool defer_reduce = false) {
   const SkinnyPlan p = plan_skinny(jobs, n);
   GemmReq q[2];
   ReduceJob rj[2];
+  // in-kernel fix-up needs one counter per output tile of each job
+  int64_t tiles_total = 0;
+  for (int i = 0; i < n; ++i)
+    tiles_total += ((jobs[i].rows + kBM - 1) / kBM) * (p.Npad[i] / p.BN[i]);
+  const bool fixup = !p.direct && c.fixup_enabled() && tiles_total <= Ctx::kCounterCap;
+  int64_t ctr_off = 0;
   for (int i = 0; i < n; ++i) {
     const Skinny& j = jobs[i];
     q[i] = base_req((int)j.rows, p.direct ? (int)j.r : p.Npad[i], kid);
@@ -242,6 +252,16 @@ runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, KernelI
       q[i].split_stride = j.rows * (int64_t)p.Npad[i];
       q[i].splits = p.splits[i];
       q[i].kb_per_split = p.kps[i];
+      if (fixup) {
+        q[i].counters = c.counters() + ctr_off;
+        ctr_off += ((j.rows + kBM - 1) / kBM) * (p.Npad[i] / p.BN[i]);
+        q[i].fix_cols = (int)j.r;
+        q[i].fix_out = j.out;
+        q[i].fix_ldo = j.ldo;
+        q[i].fix_bf16 = j.out_bf16 ? 1 : 0;
+        q[i].fix_transpose = j.transpose ? 1 : 0;
+        q[i].fix_accumulate = j.accumulate ? 1 : 0;
+      }
     }
     rj[i] = ReduceJob{Pi, p.splits[i], j.rows * (int64_t)p.Npad[i], (int)j.rows, (int)j.r, p.Npad[i], j.out,
                       j.out_bf16 ? 1 : 0, j.ldo, j.transpose ? 1 : 0, j.accumulate ? 1 : 0};
@@ -249,9 +269,19 @@ runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, KernelI
   std::string err;
   cudaError_t e = launch_tc_gemm(c, q, n, st, &err);
   if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
-  if (!p.direct) {
-    e = launch_splitk_reduce(c, rj, n, st);
+  if (!p.direct && !fixup) {
+    cudaStream_t rs = st;
+    if (defer_reduce) {
+      rs = c.side_stream();
+      cudaEventRecord(c.fork_event(), st);
+      cudaStreamWaitEvent(rs, c.fork_event(), 0);
+    }
+    e = launch_splitk_reduce(c, rj, n, rs);
     if (e != cudaSuccess) return cuda_fail(e, "splitk_reduce launch");
+    if (defer_reduce) {
+      cudaEventRecord(c.join_event(), rs);
+      c.join_pending = true;
+    }
   }
   return RUNLORA_OK;
 }
@@ -394,13 +424,14 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
 }
 
 runlora_status_t params_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* X, const void* A, const void* B,
-                             const void* dY, void* dA, void* dB, bool gb, bool acc, Bufs& b, cudaStream_t st) {
+                             const void* dY, void* dA, void* dB, bool gb, bool acc, Bufs& b, cudaStream_t st,
+                             bool defer = false) {
   const int64_t n = s.n, k = s.k, m = s.m;
   if (v == 1 || v == 5) {  // Alg. 1 / Alg. 5: Z1, Z2 | dA = Xᵀ·Z1, dB = Z2ᵀ·dY
     Skinny pj[2] = {job_Z1(s, dY, B, b.z1), job_Z2(s, X, A, b.z2)};
     RL_TRY(run_skinny(c, pj, 2, b.P, KID_GEMM_PROJ, st));
     Skinny tj[2] = {job_dA_tok(s, X, b.z1, dA, gb, acc), job_dB_tok(s, dY, b.z2, dB, gb, acc)};
-    return run_skinny(c, tj, 2, b.P, KID_GEMM_TOKRED, st);
+    return run_skinny(c, tj, 2, b.P, KID_GEMM_TOKRED, st, defer);
   }
   if (v == 2 || v == 3) {  // Z1 = dY·Bᵀ
     Skinny j = job_Z1(s, dY, B, b.z1);
@@ -422,11 +453,11 @@ runlora_status_t params_bf16(Ctx& c, int v, const runlora_shape_t& s, const void
   }
   if (v == 2) {  // dA = Xᵀ·Z1, dB = Aᵀ·Z2'
     Skinny j[2] = {job_dA_tok(s, X, b.z1, dA, gb, acc), job_dB_dense(s, b.wp, A, dB, gb, acc)};
-    return run_skinny(c, j, 2, b.P, KID_GEMM_SMALL, st);
+    return run_skinny(c, j, 2, b.P, KID_GEMM_SMALL, st, defer);
   }
   // v = 3, 4: dA = Z2'·Bᵀ, dB = Aᵀ·Z2'
   Skinny j[2] = {job_dA_dense(s, b.wp, B, dA, gb, acc), job_dB_dense(s, b.wp, A, dB, gb, acc)};
-  return run_skinny(c, j, 2, b.P, KID_GEMM_SMALL, st);
+  return run_skinny(c, j, 2, b.P, KID_GEMM_SMALL, st, defer);  // the reducer reads only the slabs
 }
 
 runlora_status_t input_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* W, const void* A, const void* B,
@@ -545,7 +576,7 @@ runlora_status_t check_bwd_common(runlora_handle_t h, int bwd, const runlora_sha
 
 runlora_status_t do_params(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X, const void* W,
                            const void* A, const void* B, const void* dY, void* dA, void* dB, int grad_dtype,
-                           int accumulate, void* ws, size_t ws_bytes, void* stream) {
+                           int accumulate, void* ws, size_t ws_bytes, void* stream, bool defer = false) {
   RL_TRY(check_bwd_common(h, bwd, s));
   (void)W;
   RL_TRY(check_ptr(X, "X"));
@@ -562,7 +593,8 @@ runlora_status_t do_params(runlora_handle_t h, int bwd, const runlora_shape_t* s
   DeviceGuard dg(h->ctx->device());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (s->dtype == RUNLORA_BF16)
-    RL_TRY(params_bf16(*h->ctx, bwd, *s, X, A, B, dY, dA, dB, grad_dtype == RUNLORA_BF16, accumulate != 0, b, st));
+    RL_TRY(params_bf16(*h->ctx, bwd, *s, X, A, B, dY, dA, dB, grad_dtype == RUNLORA_BF16, accumulate != 0, b, st,
+                       defer));
   else
     RL_TRY(params_f32(*h->ctx, bwd, *s, X, A, B, dY, dA, dB, accumulate != 0, b, st));
   return post_launch();
@@ -588,9 +620,19 @@ runlora_status_t do_input(runlora_handle_t h, int bwd, const runlora_shape_t* s,
 runlora_status_t do_backward(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X, const void* W,
                              const void* A, const void* B, const void* dY, void* dX, void* dA, void* dB,
                              int grad_dtype, int accumulate, void* ws, size_t ws_bytes, void* stream) {
-  RL_TRY(do_params(h, bwd, s, X, W, A, B, dY, dA, dB, grad_dtype, accumulate, ws, ws_bytes, stream));
-  if (dX) RL_TRY(do_input(h, bwd, s, W, A, B, dY, dX, ws, ws_bytes, stream));
-  return RUNLORA_OK;
+  // The adapter-gradient reducer runs on the side stream, overlapping the dX GEMM; the
+  // caller's stream joins it before this call's work is complete in stream order.
+  const bool defer = dX != nullptr;
+  h->ctx->join_pending = false;
+  runlora_status_t st = do_params(h, bwd, s, X, W, A, B, dY, dA, dB, grad_dtype, accumulate, ws, ws_bytes, stream,
+                                  defer);
+  if (st == RUNLORA_OK && dX) st = do_input(h, bwd, s, W, A, B, dY, dX, ws, ws_bytes, stream);
+  if (h->ctx->join_pending) {
+    DeviceGuard dg(h->ctx->device());
+    cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), h->ctx->join_event(), 0);
+    h->ctx->join_pending = false;
+  }
+  return st;
 }
 
 // ------------------------------------------------------------ selector

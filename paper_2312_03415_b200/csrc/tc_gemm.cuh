@@ -57,6 +57,14 @@ struct Prob {
   const __nv_bfloat16* Cin;  // OUT_BF16_ADD: added matrix [M, ldc]
   long long ldc;
   uint64_t hint_a, hint_b;   // TMA L2 cache hints
+  // Split-K fix-up (OUT_F32 with counters != nullptr): the LAST unit of an output tile to
+  // finish sums the fp32 slabs of all splits in fixed split order (deterministic) and
+  // writes the final out (fp32/bf16, optionally transposed/accumulated); counters self-reset.
+  int* counters;
+  int fix_cols;              // valid output columns (r)
+  void* fix_out;
+  long long fix_ldo;
+  int fix_bf16, fix_transpose, fix_accumulate;
 };
 
 struct GemmArgs {
@@ -80,7 +88,7 @@ struct TileCfg {
   static constexpr uint32_t B_BYTES = (BN_MAX / CG) * kBK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = (2 * BN_MAX <= 32) ? 32 : (2 * BN_MAX <= 64) ? 64
                                         : (2 * BN_MAX <= 128) ? 128 : (2 * BN_MAX <= 256) ? 256 : 512;
   static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
@@ -161,6 +169,57 @@ __device__ __forceinline__ void store_row_segment(const Prob& p, int split, int 
   }
 }
 
+// Epilogue warps (4..7, 128 threads) only: named barrier 1.
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// Deterministic split-K fix-up, run by the 128 epilogue threads after their unit's fp32
+// slab is stored: the last-arriving unit of the tile reduces all slabs in split order.
+__device__ __forceinline__ void splitk_fixup(const Prob& p, const Unit& t, int m0, int n0, int row, int* s_flag) {
+  __threadfence();
+  epi_bar();
+  const int tile = t.m_blk * p.num_n_tiles + t.n_blk;
+  if (threadIdx.x == 4 * 32) {
+    const int old = atomicAdd(&p.counters[tile], 1);
+    *s_flag = (old == p.num_splits - 1) ? 1 : 0;
+  }
+  epi_bar();
+  const int last = *s_flag;
+  epi_bar();  // everyone has read the flag before it can be rewritten for the next unit
+  if (!last) return;
+  __threadfence();
+  if (row < p.M) {
+    const int c_end = min(n0 + p.bn, p.fix_cols);
+    for (int c = n0; c < c_end; c += 4) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float* src = static_cast<const float*>(p.D) + (long long)row * p.ldd + c;
+      for (int sp = 0; sp < p.num_splits; ++sp) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(src + sp * p.split_stride));
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+      const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (c + e >= c_end) break;
+        const long long o = p.fix_transpose ? (long long)(c + e) * p.fix_ldo + row : (long long)row * p.fix_ldo + c + e;
+        float v = a4[e];
+        if (p.fix_bf16) {
+          __nv_bfloat16* d = static_cast<__nv_bfloat16*>(p.fix_out) + o;
+          if (p.fix_accumulate) v += __bfloat162float(*d);
+          *d = __float2bfloat16_rn(v);
+        } else {
+          float* d = static_cast<float*>(p.fix_out) + o;
+          if (p.fix_accumulate) v += *d;
+          *d = v;
+        }
+      }
+    }
+  }
+  if (threadIdx.x == 4 * 32) p.counters[tile] = 0;  // ready for the next launch
+}
+
 template <int BN_MAX, int CG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_gemm_kernel(const __grid_constant__ Tmaps tm, const __grid_constant__ GemmArgs g) {
@@ -178,6 +237,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
+  __shared__ int s_flag[1];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -317,11 +377,51 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int n0 = t.n_blk * p.bn;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
+      const int row = (g.dbg == 3) ? 0x7fffffff : m0 + q * 32 + lane;
+      // W + A·B (K = r is tiny, so the epilogue is the whole cost): fetch this row's
+      // 256-column segment of W before waiting for the accumulator, all 32 loads in flight.
+      const bool add256 = p.out_mode == OUT_BF16_ADD && p.bn == 256 && BN_MAX == 256;
+      uint4 cin[32];
+      if (add256) {
+        const __nv_bfloat16* src = p.Cin + (long long)row * p.ldc + n0;
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          cin[e] = (row < p.M && n0 + 8 * e < p.N) ? __ldg(reinterpret_cast<const uint4*>(src) + e) : make_uint4(0, 0, 0, 0);
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = (g.dbg == 3) ? 0x7fffffff : m0 + q * 32 + lane;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN_MAX;
       if (g.dbg == 4) {
+      } else if (add256) {
+#pragma unroll
+        for (int c8 = 0; c8 < 8; ++c8) {
+          if (n0 + c8 * 32 >= p.N) break;  // warp-uniform
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_row + c8 * 32, v);
+          tmem_ld_wait();
+          if (row < p.M) {
+            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.D) + (long long)row * p.ldd + n0 + c8 * 32;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              if (n0 + c8 * 32 + 8 * e < p.N) {
+                const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&cin[c8 * 4 + e]);
+                float f[8];
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                  const float2 cf = __bfloat1622float2(c2[x]);
+                  f[2 * x] = __uint_as_float(v[8 * e + 2 * x]) + cf.x;
+                  f[2 * x + 1] = __uint_as_float(v[8 * e + 2 * x + 1]) + cf.y;
+                }
+                uint4 o;
+                o.x = pack_bf16x2(f[0], f[1]);
+                o.y = pack_bf16x2(f[2], f[3]);
+                o.z = pack_bf16x2(f[4], f[5]);
+                o.w = pack_bf16x2(f[6], f[7]);
+                *reinterpret_cast<uint4*>(dst + 8 * e) = o;
+              }
+            }
+          }
+        }
       } else if (p.bn % 32 == 0) {
 #pragma unroll 1
         for (int c = 0; c < p.bn; c += 32) {
@@ -344,6 +444,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote<CG>(&tempty[acc], 0);  // leader's barrier
+      if (p.counters) splitk_fixup(p, t, m0, n0, row, s_flag);
     }
   }
   tc_fence_before();
