@@ -20,10 +20,26 @@ namespace {
 
 constexpr int kMaxDevices = 64;
 
-template <int BN, int CG>
+// Plain launch with the programmatic-dependent-launch attribute (when enabled).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(Ctx& ctx, void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = ctx.pdl() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+template <int BN, int CG, int OCC = 1, bool WADD = false>
 cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, const GemmArgs& g, cudaStream_t s) {
-  auto kern = tc_gemm_kernel<BN, CG>;
-  constexpr uint32_t smem = TileCfg<BN, CG>::SMEM_BYTES;
+  auto kern = tc_gemm_kernel<BN, CG, OCC, WADD>;
+  constexpr uint32_t smem = TileCfg<BN, CG, OCC>::SMEM_BYTES;
   static bool attr_set[kMaxDevices] = {};
   const int dev = ctx.device();
   if (dev < kMaxDevices && !attr_set[dev]) {
@@ -31,30 +47,48 @@ cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, const GemmArgs& g, cudaStream_t s)
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
   }
-  const int groups_max = ctx.num_sms() / CG;
+  const int groups_max = ctx.num_sms() * OCC / CG;
   const int groups = g.total_units < groups_max ? g.total_units : groups_max;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(groups * CG);
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  int na = 0;
   if (CG > 1) {
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = CG;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
   }
+  if (ctx.pdl()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, kern, tm, g);
 }
 
-cudaError_t dispatch_tc(Ctx& ctx, int bn_max, int cg, const Tmaps& tm, const GemmArgs& g, cudaStream_t s) {
+cudaError_t dispatch_tc(Ctx& ctx, int bn_max, int cg, bool occ2, const Tmaps& tm, const GemmArgs& g,
+                        cudaStream_t s) {
+  if (cg == 1 && bn_max == 256 && g.p[0].out_mode == OUT_BF16_ADD) return run_tc<256, 1, 1, true>(ctx, tm, g, s);
   if (cg == 2) {
     if (bn_max == 256) return run_tc<256, 2>(ctx, tm, g, s);
     if (bn_max == 128) return run_tc<128, 2>(ctx, tm, g, s);
     return cudaErrorInvalidValue;
+  }
+  if (occ2) {
+    switch (bn_max) {
+      case 16: return run_tc<16, 1, 2>(ctx, tm, g, s);
+      case 32: return run_tc<32, 1, 2>(ctx, tm, g, s);
+      case 48: return run_tc<48, 1, 2>(ctx, tm, g, s);
+      case 64: return run_tc<64, 1, 2>(ctx, tm, g, s);
+      default: break;
+    }
   }
   switch (bn_max) {
     case 16: return run_tc<16, 1>(ctx, tm, g, s);
@@ -76,7 +110,9 @@ struct ReduceArgs {
 // One thread per (row i, 4-column group): float4 loads of every split slab in fixed
 // split order (deterministic), 4 slabs in flight at a time.  Column groups vary fastest
 // so a warp reads contiguous 512 B of each slab.
-__global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constant__ ReduceArgs a) {
+__global__ void __launch_bounds__(256, 4) splitk_reduce_kernel(const __grid_constant__ ReduceArgs a) {
+  pdl_wait();
+  pdl_launch_dependents();
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < a.total;
        idx += (long long)gridDim.x * blockDim.x) {
     const bool second = idx >= a.total0;
@@ -88,13 +124,13 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
     const float4* p = reinterpret_cast<const float4*>(J.P + (long long)i * J.ldp + c0);
     const long long st4 = J.split_stride / 4;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s0 = 0; s0 < J.splits; s0 += 16) {
-      float4 v[16];  // up to 16 slabs in flight, then summed in split order
+    for (int s0 = 0; s0 < J.splits; s0 += 8) {
+      float4 v[8];  // up to 8 slabs in flight, then summed in split order
 #pragma unroll
-      for (int x = 0; x < 16; ++x)
+      for (int x = 0; x < 8; ++x)
         if (s0 + x < J.splits) v[x] = __ldg(p + (s0 + x) * st4);
 #pragma unroll
-      for (int x = 0; x < 16; ++x) {
+      for (int x = 0; x < 8; ++x) {
         if (s0 + x < J.splits) {
           acc.x += v[x].x;
           acc.y += v[x].y;
@@ -131,6 +167,8 @@ __global__ void __launch_bounds__(256) sgemm_kernel(int M, int N, int K, const f
                                                     int accumulate) {
   __shared__ float As[16][64 + 4];
   __shared__ float Bs[16][64 + 4];
+  pdl_wait();
+  pdl_launch_dependents();
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
   float c[4][4] = {};
@@ -229,6 +267,7 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
     p.b_mn = r.b_mn;
     p.b_swz = b_swz;
     p.a_3d = a3 ? 1 : 0;
+    p.rotate = r.rotate_k ? 1 : 0;
     p.b_3d = b3 ? 1 : 0;
     p.out_mode = r.out_mode;
     p.idesc = idesc_bf16(kBM * cg, r.BN, r.a_mn, r.b_mn);
@@ -255,7 +294,7 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
   if (nreq == 1) g.p[1] = g.p[0], g.p[1].units = 0;
   if (g.total_units <= 0) return cudaSuccess;
   ctx.launch_begin(s, reqs[0].kid);
-  cudaError_t e = dispatch_tc(ctx, bn_max, cg, tm, g, s);
+  cudaError_t e = dispatch_tc(ctx, bn_max, cg, ctx.occ2() && reqs[0].a_stream_once, tm, g, s);
   ctx.launch_end(s);
   if (e != cudaSuccess && err) *err = std::string("tc_gemm launch: ") + cudaGetErrorString(e);
   return e;
@@ -276,9 +315,9 @@ cudaError_t launch_splitk_reduce(Ctx& ctx, const ReduceJob* jobs, int njobs, cud
   const long long cap = (long long)ctx.num_sms() * 16;
   if (blocks > cap) blocks = cap;
   ctx.launch_begin(s, KID_SPLITK_REDUCE);
-  splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>(a);
+  cudaError_t e = launch_pdl(ctx, splitk_reduce_kernel, dim3((unsigned)blocks), dim3(256), s, a);
   ctx.launch_end(s);
-  return cudaGetLastError();
+  return e;
 }
 
 cudaError_t launch_sgemm(Ctx& ctx, int M, int N, int K, const float* A, int64_t sa0, int64_t sa1, const float* B,
@@ -286,9 +325,11 @@ cudaError_t launch_sgemm(Ctx& ctx, int M, int N, int K, const float* A, int64_t 
                          bool accumulate, cudaStream_t s) {
   dim3 grid((N + 63) / 64, (M + 63) / 64);
   ctx.launch_begin(s, KID_SGEMM_F32);
-  sgemm_kernel<<<grid, 256, 0, s>>>(M, N, K, A, sa0, sa1, B, sb0, sb1, C, ldc, Cadd, ldadd, accumulate ? 1 : 0);
+  cudaError_t e = launch_pdl(ctx, sgemm_kernel, grid, dim3(256), s, M, N, K, A, (long long)sa0, (long long)sa1, B,
+                             (long long)sb0, (long long)sb1, C, (long long)ldc, Cadd, (long long)ldadd,
+                             accumulate ? 1 : 0);
   ctx.launch_end(s);
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace runlora

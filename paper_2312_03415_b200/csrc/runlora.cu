@@ -176,21 +176,14 @@ SkinnyPlan plan_skinny(const Skinny* jobs, int n) {
     kb_max = std::max<int64_t>(kb_max, (jobs[i].K + kBK - 1) / kBK);
     direct_ok = direct_ok && can_direct(jobs[i]);
   }
-  // enough row tiles (>= 2/3 of the SMs busy) -> no split, direct bf16 epilogue
+  // enough row tiles (>= 2/3 of the SMs busy) -> no split, direct bf16 epilogue;
+  // otherwise the smallest split that fills one wave of CTA slots (2 per SM for these
+  // HBM-bound kernels): fewer splits = smaller fp32 slabs and a cheaper reducer.
   p.direct = direct_ok && 3 * tiles >= 2 * kSmTarget;
   int64_t s = 1;
   if (!p.direct) {
-    // choose the split count minimising (waves x k-blocks per unit) + a partial-traffic term
-    double best = 1e30;
-    for (int64_t c = 1; c <= kMaxSplits && c <= kb_max; ++c) {
-      const int64_t units = tiles * c;
-      const int64_t waves = (units + kSmTarget - 1) / kSmTarget;
-      const double cost = (double)waves * (double)((kb_max + c - 1) / c) + 0.25 * (double)c;
-      if (cost < best - 1e-9) {
-        best = cost;
-        s = c;
-      }
-    }
+    s = std::max<int64_t>(1, (2 * kSmTarget) / std::max<int64_t>(tiles, 1));
+    s = std::min<int64_t>(s, std::min<int64_t>(kMaxSplits, kb_max));
   }
   size_t off = 0;
   for (int i = 0; i < n; ++i) {
@@ -240,6 +233,7 @@ runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, KernelI
     q[i].K1 = (int)j.K;
     q[i].BN = p.BN[i];
     q[i].a_stream_once = true;
+    q[i].rotate_k = c.rotate_k();
     float* Pi = reinterpret_cast<float*>(reinterpret_cast<char*>(P) + p.p_off[i]);
     if (p.direct) {
       q[i].out_mode = OUT_BF16;
@@ -910,6 +904,7 @@ extern "C" runlora_status_t runlora_debug_gemm(runlora_handle_t h, int M, int N,
   if (M <= 0 || N <= 0 || K1 <= 0 || K2 < 0 || splits < 1) return fail(RUNLORA_ERR_INVALID_ARG, "bad gemm dims");
   GemmReq q = base_req(M, N, KID_GEMM_MAIN);
   q.cg = cg == 2 ? 2 : 1;
+  q.a_stream_once = BN <= 64;  // rank-r style problem: eligible for the 2-CTA/SM variant
   q.a = a_mn ? mat(A1, K1, M) : mat(A1, M, K1);
   q.a_mn = a_mn != 0;
   q.b = b_mn ? mat(B1, K1, N) : mat(B1, N, K1);

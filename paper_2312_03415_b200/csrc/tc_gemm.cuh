@@ -48,6 +48,7 @@ struct Prob {
   int a_mn, b_mn;        // operand majorness (0 = K-major)
   int b_swz;             // MN-major B swizzle width in bytes (32, 64, 128); K-major operands use 128
   int a_3d, b_3d;        // MN-major operand loaded by one 3-D TMA box (all swizzle chunks at once)
+  int rotate;            // start each unit's K walk at a unit-dependent block (see producer)
   int out_mode;          // OutMode
   uint32_t idesc;        // tcgen05 instruction descriptor
   uint32_t stage_tx;     // TMA bytes per stage for the whole CTA group
@@ -82,12 +83,13 @@ constexpr int kBM = 128;  // rows per CTA
 constexpr int kBK = 64;
 constexpr int kGemmThreads = 256;
 
-template <int BN_MAX, int CG>
+// OCC = CTAs per SM (2 for the HBM-bound rank-r kernels: twice the TMA requests in flight).
+template <int BN_MAX, int CG, int OCC = 1>
 struct TileCfg {
   static constexpr uint32_t A_BYTES = kBM * kBK * 2;
   static constexpr uint32_t B_BYTES = (BN_MAX / CG) * kBK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES_RAW = (200 * 1024 / OCC) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = (2 * BN_MAX <= 32) ? 32 : (2 * BN_MAX <= 64) ? 64
                                         : (2 * BN_MAX <= 128) ? 128 : (2 * BN_MAX <= 256) ? 256 : 512;
@@ -220,10 +222,11 @@ __device__ __forceinline__ void splitk_fixup(const Prob& p, const Unit& t, int m
   if (threadIdx.x == 4 * 32) p.counters[tile] = 0;  // ready for the next launch
 }
 
-template <int BN_MAX, int CG>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+// WADD: instantiation for W + A·B (prefetches the 256-column W segment of each row).
+template <int BN_MAX, int CG, int OCC = 1, bool WADD = false>
+__global__ void __launch_bounds__(kGemmThreads, OCC)
     tc_gemm_kernel(const __grid_constant__ Tmaps tm, const __grid_constant__ GemmArgs g) {
-  using C = TileCfg<BN_MAX, CG>;
+  using C = TileCfg<BN_MAX, CG, OCC>;
   constexpr int STAGES = C::STAGES;
   static_assert(BN_MAX % (16 * CG) == 0 && BN_MAX >= 16 && BN_MAX <= 256, "UMMA N");
 
@@ -265,6 +268,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // everything above overlapped the previous kernel's tail (PDL); inputs are read below
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -281,6 +287,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int kb1 = min(p.nk1, kb0 + p.kb_per_split);
       const int nmain = kb1 - kb0;
       const int nkb = nmain + (t.split == 0 ? p.nk2 : 0);
+      const int rot = nmain > 1 ? (int)(((unsigned)u * 7919u) % (unsigned)nmain) : 0;
       if (g.dbg == 1 || g.dbg >= 3) continue;
       const int cw = p.b_swz >> 1;   // MN-major B chunk width (elements)
       const int cb = p.b_swz * kBK;  // MN-major B chunk bytes (64 K-rows)
@@ -294,7 +301,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const bool tail = i >= nmain;
           const CUtensorMap* ta = &tm.m[t.prob][tail ? 2 : 0];
           const CUtensorMap* tb = &tm.m[t.prob][tail ? 3 : 1];
-          const int kc = (tail ? (i - nmain) : (kb0 + i)) * kBK;
+          // p.rotate: each unit starts its K walk at a different block so that concurrently
+          // running CTAs do not all hit the same column offset of their rows (DRAM channel
+          // camping on streams with power-of-two row pitch)
+          const int ki = (p.rotate && nmain > 1) ? (i + rot) % nmain : i;
+          const int kc = (tail ? (i - nmain) : (kb0 + ki)) * kBK;
           if (!p.a_mn) {
             tma_load_2d<CG>(ta, fb, a, kc, m0, p.hint_a);
           } else if (p.a_3d) {
@@ -332,6 +343,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int kb1 = min(p.nk1, kb0 + p.kb_per_split);
       const int nmain = kb1 - kb0;
       const int nkb = nmain + (t.split == 0 ? p.nk2 : 0);
+      const int rot = nmain > 1 ? (int)(((unsigned)u * 7919u) % (unsigned)nmain) : 0;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -345,7 +357,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int i = 0; i < nkb; ++i) {
         if (g.dbg != 1 && g.dbg < 3) mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const int kleft = (i < nmain) ? (p.k1 - (kb0 + i) * kBK) : (p.k2 - (i - nmain) * kBK);
+        const int ki = (p.rotate && nmain > 1) ? (i + rot) % nmain : i;
+        const int kleft = (i < nmain) ? (p.k1 - (kb0 + ki) * kBK) : (p.k2 - (i - nmain) * kBK);
         const int ksteps = min(kBK / 16, (kleft + 15) >> 4);
         const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
         const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
@@ -380,8 +393,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int row = (g.dbg == 3) ? 0x7fffffff : m0 + q * 32 + lane;
       // W + A·B (K = r is tiny, so the epilogue is the whole cost): fetch this row's
       // 256-column segment of W before waiting for the accumulator, all 32 loads in flight.
-      const bool add256 = p.out_mode == OUT_BF16_ADD && p.bn == 256 && BN_MAX == 256;
-      uint4 cin[32];
+      const bool add256 = WADD && p.out_mode == OUT_BF16_ADD && p.bn == 256 && BN_MAX == 256;
+      uint4 cin[WADD ? 32 : 1];
       if (add256) {
         const __nv_bfloat16* src = p.Cin + (long long)row * p.ldc + n0;
 #pragma unroll

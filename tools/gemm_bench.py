@@ -52,6 +52,7 @@ def main():
     ap.add_argument("--a-mn", action="store_true")
     ap.add_argument("--b-mn", action="store_true")
     ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--splits", type=int, default=1)
     ap.add_argument("--cublas", action="store_true")
     ap.add_argument("--sustain", type=float, default=0.0, help="also run back-to-back for this many seconds, "
                     "sampling SM clock and power")
@@ -68,14 +69,15 @@ def main():
     A2 = torch.randn(M, max(a.K2, 8), device="cuda", dtype=bf)
     B2 = torch.randn(max(a.K2, 8), N, device="cuda", dtype=bf) if a.b_mn else \
         torch.randn(N, max(a.K2, 8), device="cuda", dtype=bf)
-    D = torch.empty(M, N, device="cuda", dtype=bf)
+    D = torch.empty(M, N, device="cuda", dtype=bf) if a.splits == 1 else \
+        torch.empty(a.splits, M, N, device="cuda", dtype=torch.float32)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     flops = 2.0 * M * N * (K + a.K2)
     for cg in a.cg:
         def run():
             st = f(h._h, M, N, K, A.data_ptr(), int(a.a_mn), B.data_ptr(), int(a.b_mn), a.K2, A2.data_ptr(),
-                   B2.data_ptr(), 0, D.data_ptr(), None, a.bn, 1, cg, s)
+                   B2.data_ptr(), 0 if a.splits == 1 else 2, D.data_ptr(), None, a.bn, a.splits, cg, s)
             assert st == 0, rl._lib.runlora_last_error()
         for _ in range(5):
             run()
@@ -90,7 +92,8 @@ def main():
             ts.append(e0.elapsed_time(e1))
         ts.sort()
         med = ts[len(ts) // 2]
-        rec = {"kernel": "tc_gemm", "cg": cg, "bn": a.bn, "M": M, "N": N, "K": K, "K2": a.K2,
+        rec = {"kernel": "tc_gemm", "cg": cg, "bn": a.bn, "M": M, "N": N, "K": K, "K2": a.K2, "splits": a.splits,
+               "GBps_A": (M * K * 2) / (med * 1e-3) / 1e9,
                "a_mn": a.a_mn, "b_mn": a.b_mn, "median_us": med * 1e3, "min_us": ts[0] * 1e3,
                "tflops_median": flops / (med * 1e-3) / 1e12}
         if a.sustain:
