@@ -25,6 +25,7 @@ Ctx::Ctx(int device) : device_(device) {
   if (const char* e = getenv("RUNLORA_ROTATE_K")) rotate_k_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_OCC2")) occ2_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_PDL")) pdl_ = atoi(e) != 0;
+  if (const char* e = getenv("RUNLORA_L2PROMO_MN")) promo_mn_ = (CUtensorMapL2promotion)atoi(e);
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
@@ -98,7 +99,8 @@ bool Ctx::tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* 
   CUresult r = reinterpret_cast<EncodeTiledFn>(encode_fn_)(
       &tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(m.ptr), dims, strides, box, estr,
       CU_TENSOR_MAP_INTERLEAVE_NONE,
-      swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+      (chunks > 0 ? promo_mn_ : CU_TENSOR_MAP_L2_PROMOTION_L2_256B),
       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     if (err) {

@@ -110,7 +110,8 @@ class Ctx {
   bool fixup_ = false;     // env RUNLORA_SPLITK_FIXUP=1: in-kernel fix-up instead of the reducer launch
   bool rotate_k_ = false;  // env RUNLORA_ROTATE_K=1: rotated K walks (measured slower on C2)
   bool occ2_ = true;
-  bool pdl_ = true;       // env RUNLORA_OCC2=0: one CTA per SM for the rank-r kernels too
+  bool pdl_ = true;
+  CUtensorMapL2promotion promo_mn_ = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;  // 3-D (MN-major) boxes       // env RUNLORA_OCC2=0: one CTA per SM for the rank-r kernels too
   void* encode_fn_ = nullptr;
   std::mutex tmap_mu_;
   std::unordered_map<std::string, CUtensorMap> tmaps_;

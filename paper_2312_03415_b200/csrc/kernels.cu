@@ -237,8 +237,9 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
     // MN-major operands whose contiguous extent is a whole number of swizzle chunks are
     // fetched with ONE 3-D TMA box per stage instead of one 2-D box per chunk.
     const int b_cw = b_swz / 2;
-    const bool a3 = r.a_mn && r.a.cols % 64 == 0 && (r.K2 == 0 || r.a2.cols % 64 == 0);
-    const bool b3 = r.b_mn && nb > b_cw && r.b.cols % b_cw == 0 && (r.K2 == 0 || r.b2.cols % b_cw == 0);
+    static const bool tma3d = getenv("RUNLORA_TMA3D") == nullptr || atoi(getenv("RUNLORA_TMA3D")) != 0;
+    const bool a3 = tma3d && r.a_mn && r.a.cols % 64 == 0 && (r.K2 == 0 || r.a2.cols % 64 == 0);
+    const bool b3 = tma3d && r.b_mn && nb > b_cw && r.b.cols % b_cw == 0 && (r.K2 == 0 || r.b2.cols % b_cw == 0);
     if (!ctx.tmap(r.a, a_box, &tm.m[q][0], err, 128, a3 ? 2 : 0) ||
         !ctx.tmap(r.b, b_box, &tm.m[q][1], err, b_swz, b3 ? nb / b_cw : 0))
       return cudaErrorInvalidValue;
@@ -268,6 +269,9 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
     p.b_swz = b_swz;
     p.a_3d = a3 ? 1 : 0;
     p.rotate = r.rotate_k ? 1 : 0;
+    // all of B (N x K bf16) above ~48 MB -> banded raster (see decode_unit)
+    const double b_bytes = 2.0 * (double)r.N * (double)(r.K1 + r.K2);
+    p.raster_g = b_bytes > 48e6 ? 8 : 1;
     p.b_3d = b3 ? 1 : 0;
     p.out_mode = r.out_mode;
     p.idesc = idesc_bf16(kBM * cg, r.BN, r.a_mn, r.b_mn);

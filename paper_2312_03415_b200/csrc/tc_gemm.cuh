@@ -49,6 +49,7 @@ struct Prob {
   int b_swz;             // MN-major B swizzle width in bytes (32, 64, 128); K-major operands use 128
   int a_3d, b_3d;        // MN-major operand loaded by one 3-D TMA box (all swizzle chunks at once)
   int rotate;            // start each unit's K walk at a unit-dependent block (see producer)
+  int raster_g;          // output tiles are visited in bands of raster_g row tiles (1: row-major)
   int out_mode;          // OutMode
   uint32_t idesc;        // tcgen05 instruction descriptor
   uint32_t stage_tx;     // TMA bytes per stage for the whole CTA group
@@ -89,7 +90,8 @@ struct TileCfg {
   static constexpr uint32_t A_BYTES = kBM * kBK * 2;
   static constexpr uint32_t B_BYTES = (BN_MAX / CG) * kBK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (200 * 1024 / OCC) / STAGE_BYTES;
+  // up to ~225 KB of the 227 KB opt-in smem per SM (7 stages for the 256x256 pair tiles)
+  static constexpr int STAGES_RAW = ((OCC == 1 ? 225 : 110) * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = (2 * BN_MAX <= 32) ? 32 : (2 * BN_MAX <= 64) ? 64
                                         : (2 * BN_MAX <= 128) ? 128 : (2 * BN_MAX <= 256) ? 256 : 512;
@@ -107,10 +109,21 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& g, int u) {
     t.prob = 1;
   }
   const Prob& p = g.p[t.prob];
-  t.n_blk = u % p.num_n_tiles;
-  const int q = u / p.num_n_tiles;
-  t.m_blk = q % p.num_m_tiles;
-  t.split = q / p.num_m_tiles;
+  const int per_split = p.num_m_tiles * p.num_n_tiles;
+  t.split = u / per_split;
+  int r = u - t.split * per_split;
+  // Grouped raster: bands of G row tiles, row index fastest inside a band, so the CTAs
+  // resident at any time cover a compact block of the output and the A and B tiles they
+  // stream stay in L2 (walking whole rows of tiles streams all of B through L2 once per
+  // wave, e.g. an 86 MiB W for the 11008-wide Llama MLP).  G = 1 (row-major walk) when
+  // all of B fits comfortably in L2.
+  const int G = p.raster_g;
+  const int band = r / (G * p.num_n_tiles);
+  const int m_first = band * G;
+  const int g_rows = min(G, p.num_m_tiles - m_first);
+  r -= band * G * p.num_n_tiles;
+  t.m_blk = m_first + r % g_rows;
+  t.n_blk = r / g_rows;
   return t;
 }
 
