@@ -25,6 +25,7 @@ Ctx::Ctx(int device) : device_(device) {
   if (const char* e = getenv("RUNLORA_ROTATE_K")) rotate_k_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_OCC2")) occ2_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_PDL")) pdl_ = atoi(e) != 0;
+  if (const char* e = getenv("RUNLORA_WPRIME_T")) wprime_t_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_L2PROMO_MN")) promo_mn_ = (CUtensorMapL2promotion)atoi(e);
   int prev = -1;
   cudaGetDevice(&prev);
@@ -82,7 +83,7 @@ bool Ctx::tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* 
     if (err) *err = "cuTensorMapEncodeTiled entry point unavailable";
     return false;
   }
-  const cuuint32_t w = (cuuint32_t)(swz / 2);
+  const cuuint32_t w = swz == 0 ? 128u : (cuuint32_t)(swz / 2);  // swz 0: no swizzle, 256-byte rows
   cuuint64_t dims[3] = {(cuuint64_t)m.cols, (cuuint64_t)m.rows, 1};
   cuuint64_t strides[2] = {(cuuint64_t)m.ld * 2, 0};
   cuuint32_t box[3] = {w, (cuuint32_t)box_rows, 1};
@@ -99,7 +100,10 @@ bool Ctx::tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* 
   CUresult r = reinterpret_cast<EncodeTiledFn>(encode_fn_)(
       &tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(m.ptr), dims, strides, box, estr,
       CU_TENSOR_MAP_INTERLEAVE_NONE,
-      swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+      swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+      : swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+      : swz == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                  : CU_TENSOR_MAP_SWIZZLE_NONE,
       (chunks > 0 ? promo_mn_ : CU_TENSOR_MAP_L2_PROMOTION_L2_256B),
       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {

@@ -76,7 +76,8 @@ class Ctx {
   bool fixup_enabled() const { return counters_ != nullptr && fixup_; }
   bool rotate_k() const { return rotate_k_; }
   bool occ2() const { return occ2_; }
-  bool pdl() const { return pdl_; }    // programmatic dependent launch (env RUNLORA_PDL=0 disables)  // 2 CTAs/SM for rank-r kernels (env RUNLORA_OCC2=0 disables)
+  bool pdl() const { return pdl_; }
+  bool wprime_t() const { return wprime_t_; }  // forward2 builds W'ᵀ (env RUNLORA_WPRIME_T=0 disables)    // programmatic dependent launch (env RUNLORA_PDL=0 disables)  // 2 CTAs/SM for rank-r kernels (env RUNLORA_OCC2=0 disables)
   // Side stream for small work that can overlap the next big GEMM (fork/join by events).
   cudaStream_t side_stream();
   cudaEvent_t fork_event();
@@ -111,6 +112,7 @@ class Ctx {
   bool rotate_k_ = false;  // env RUNLORA_ROTATE_K=1: rotated K walks (measured slower on C2)
   bool occ2_ = true;
   bool pdl_ = true;
+  bool wprime_t_ = true;
   CUtensorMapL2promotion promo_mn_ = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;  // 3-D (MN-major) boxes       // env RUNLORA_OCC2=0: one CTA per SM for the rank-r kernels too
   void* encode_fn_ = nullptr;
   std::mutex tmap_mu_;

@@ -36,10 +36,10 @@ cudaError_t launch_pdl(Ctx& ctx, void (*kern)(KArgs...), dim3 grid, dim3 block, 
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
-template <int BN, int CG, int OCC = 1, bool WADD = false>
+template <int BN, int CG, int OCC = 1, int EPI = 0>
 cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, const GemmArgs& g, cudaStream_t s) {
-  auto kern = tc_gemm_kernel<BN, CG, OCC, WADD>;
-  constexpr uint32_t smem = TileCfg<BN, CG, OCC>::SMEM_BYTES;
+  auto kern = tc_gemm_kernel<BN, CG, OCC, EPI>;
+  constexpr uint32_t smem = TileCfg<BN, CG, OCC, EPI>::SMEM_BYTES;
   static bool attr_set[kMaxDevices] = {};
   const int dev = ctx.device();
   if (dev < kMaxDevices && !attr_set[dev]) {
@@ -75,7 +75,9 @@ cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, const GemmArgs& g, cudaStream_t s)
 
 cudaError_t dispatch_tc(Ctx& ctx, int bn_max, int cg, bool occ2, const Tmaps& tm, const GemmArgs& g,
                         cudaStream_t s) {
-  if (cg == 1 && bn_max == 256 && g.p[0].out_mode == OUT_BF16_ADD) return run_tc<256, 1, 1, true>(ctx, tm, g, s);
+  if (cg == 1 && bn_max == 256 && g.p[0].out_mode == OUT_BF16_ADD) return run_tc<256, 1, 1, 1>(ctx, tm, g, s);
+  if (cg == 1 && bn_max == 256 && g.p[0].out_mode == OUT_BF16_ADD_T) return run_tc<256, 1, 1, 2>(ctx, tm, g, s);
+  if (g.p[0].out_mode == OUT_BF16_ADD || g.p[0].out_mode == OUT_BF16_ADD_T) return cudaErrorNotSupported;
   if (cg == 2) {
     if (bn_max == 256) return run_tc<256, 2>(ctx, tm, g, s);
     if (bn_max == 128) return run_tc<128, 2>(ctx, tm, g, s);
@@ -250,6 +252,12 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
     } else {
       tm.m[q][2] = tm.m[q][0];
       tm.m[q][3] = tm.m[q][1];
+    }
+    if (r.out_mode == OUT_BF16_ADD_T) {
+      // Cin stored [N rows][M cols] (ld = ldc): one un-swizzled {128, BN} block per tile
+      if (r.K2 > 0 || r.BN != 256 || cg != 1) return cudaErrorNotSupported;
+      const DeviceMat cm{r.Cin, (int64_t)r.N, (int64_t)r.M, r.ldc};
+      if (!ctx.tmap(cm, 256, &tm.m[q][2], err, 0)) return cudaErrorInvalidValue;
     }
     Prob& p = g.p[q];
     p.M = r.M;

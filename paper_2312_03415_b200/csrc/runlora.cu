@@ -382,6 +382,27 @@ runlora_status_t wprime_bf16(Ctx& c, const runlora_shape_t& s, const void* W, co
   return gemm(c, q, st);
 }
 
+// W'ᵀ = (W + A·B)ᵀ  (m×k, bf16) for forward2: stored K-major for the Y GEMM's B operand
+// (the tensor cores stream K-major B faster than MN-major B).  GEMM M = m,
+// N = k, K = r: A_op = Bᵀ (B stored [r, m]: MN-major), B_op = Aᵀ (A stored [k, r]:
+// K-major); the epilogue adds W transposed through shared memory.
+runlora_status_t wprime_t_bf16(Ctx& c, const runlora_shape_t& s, const void* W, const void* A, const void* B,
+                               void* Wpt, cudaStream_t st) {
+  GemmReq q = base_req((int)s.m, (int)s.k, KID_GEMM_WPRIME);
+  q.a = mat(B, s.r, s.m);
+  q.a_mn = true;
+  q.b = mat(A, s.k, s.r);
+  q.b_mn = false;
+  q.K1 = (int)s.r;
+  q.out_mode = OUT_BF16_ADD_T;
+  q.Cin = W;
+  q.ldc = s.m;
+  q.D = Wpt;
+  q.ldd = s.k;
+  q.BN = 256;
+  return gemm(c, q, st);
+}
+
 // The dominant Y / dX GEMMs: 256x256 tiles on CTA pairs (cta_group::2) unless disabled.
 GemmReq main_req(Ctx& c, int M, int N) {
   GemmReq q = base_req(M, N, KID_GEMM_MAIN);
@@ -410,6 +431,10 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
     q.a2 = mat(b.z2, n, r);
     q.b2 = mat(B, r, m);
     q.K2 = (int)r;
+  } else if (c.wprime_t()) {
+    RL_TRY(wprime_t_bf16(c, s, W, A, B, b.wp, st));  // W'ᵀ [m, k]
+    q.b = mat(b.wp, m, k);
+    q.b_mn = false;
   } else {
     RL_TRY(wprime_bf16(c, s, W, A, B, b.wp, st));
     q.b = mat(b.wp, k, m);

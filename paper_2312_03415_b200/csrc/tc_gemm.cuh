@@ -35,7 +35,9 @@
 
 namespace runlora {
 
-enum OutMode : int { OUT_BF16 = 0, OUT_BF16_ADD = 1, OUT_F32 = 2 };
+enum OutMode : int { OUT_BF16 = 0, OUT_BF16_ADD = 1, OUT_F32 = 2, OUT_BF16_ADD_T = 3 };
+// OUT_BF16_ADD:   D[i, j] = acc[i, j] + Cin[i * ldc + j]
+// OUT_BF16_ADD_T: D[i, j] = acc[i, j] + Cin[j * ldc + i]   (transposed add; EPI = 2 kernels)
 
 struct Prob {
   int M, N;              // output extent (epilogue masks rows >= M, cols >= N)
@@ -85,17 +87,19 @@ constexpr int kBK = 64;
 constexpr int kGemmThreads = 256;
 
 // OCC = CTAs per SM (2 for the HBM-bound rank-r kernels: twice the TMA requests in flight).
-template <int BN_MAX, int CG, int OCC = 1>
+// EPI = 2 (transposed add): the epilogue stages the BN x 128 block of Cin in smem.
+template <int BN_MAX, int CG, int OCC = 1, int EPI = 0>
 struct TileCfg {
   static constexpr uint32_t A_BYTES = kBM * kBK * 2;
   static constexpr uint32_t B_BYTES = (BN_MAX / CG) * kBK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t CT_BYTES = EPI == 2 ? 2 * BN_MAX * kBM * 2 : 0;  // double-buffered Cin block
   // up to ~225 KB of the 227 KB opt-in smem per SM (7 stages for the 256x256 pair tiles)
-  static constexpr int STAGES_RAW = ((OCC == 1 ? 225 : 110) * 1024) / STAGE_BYTES;
+  static constexpr int STAGES_RAW = ((OCC == 1 ? 225 : 110) * 1024 - CT_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = (2 * BN_MAX <= 32) ? 32 : (2 * BN_MAX <= 64) ? 64
                                         : (2 * BN_MAX <= 128) ? 128 : (2 * BN_MAX <= 256) ? 256 : 512;
-  static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + CT_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 struct Unit {
@@ -235,11 +239,13 @@ __device__ __forceinline__ void splitk_fixup(const Prob& p, const Unit& t, int m
   if (threadIdx.x == 4 * 32) p.counters[tile] = 0;  // ready for the next launch
 }
 
-// WADD: instantiation for W + A·B (prefetches the 256-column W segment of each row).
-template <int BN_MAX, int CG, int OCC = 1, bool WADD = false>
+// EPI = 1: W + A·B (prefetches the 256-column W segment of each row);
+// EPI = 2: (W + A·B)ᵀ written directly (transposed add through a smem block of W).
+template <int BN_MAX, int CG, int OCC = 1, int EPI = 0>
 __global__ void __launch_bounds__(kGemmThreads, OCC)
     tc_gemm_kernel(const __grid_constant__ Tmaps tm, const __grid_constant__ GemmArgs g) {
-  using C = TileCfg<BN_MAX, CG, OCC>;
+  using C = TileCfg<BN_MAX, CG, OCC, EPI>;
+  constexpr bool WADD = EPI == 1;
   constexpr int STAGES = C::STAGES;
   static_assert(BN_MAX % (16 * CG) == 0 && BN_MAX >= 16 && BN_MAX <= 256, "UMMA N");
 
@@ -252,6 +258,11 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  // EPI = 2: two Cin blocks [BN_MAX rows (output cols)][128 (output rows)] bf16 (TMA-filled
+  // by the producer, one per tile, double-buffered), then their full/empty barriers.
+  __nv_bfloat16* sCt = reinterpret_cast<__nv_bfloat16*>(smem + STAGES * C::STAGE_BYTES + 256);
+  uint64_t* ct_full = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // 2 barriers, then 2 more
+  uint64_t* ct_empty = ct_full + 2;
 
   __shared__ int s_flag[1];
   const int warp = threadIdx.x >> 5;
@@ -272,6 +283,10 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * CG);
+      if constexpr (EPI == 2) {
+        mbar_init(&ct_full[a], 1);
+        mbar_init(&ct_empty[a], 4);
+      }
     }
     fence_mbar_init();
   }
@@ -290,6 +305,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
     // The whole warp runs the loop (warp-uniform values); one elected lane issues.
     int stage = 0;
     uint32_t phase = 0;
+    int it_p = 0;  // EPI = 2: Cin block counter
     for (int u = group; u < g.total_units; u += ngroups) {
       const Unit t = decode_unit(g, u);
       const Prob& p = g.p[t.prob];
@@ -302,6 +318,17 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       const int nkb = nmain + (t.split == 0 ? p.nk2 : 0);
       const int rot = nmain > 1 ? (int)(((unsigned)u * 7919u) % (unsigned)nmain) : 0;
       if (g.dbg == 1 || g.dbg >= 3) continue;
+      if constexpr (EPI == 2) {
+        const int cb = it_p & 1;
+        mbar_wait(&ct_empty[cb], ((it_p >> 1) & 1) ^ 1);
+        if (elect_one_sync()) {
+          mbar_arrive_expect_tx(&ct_full[cb], BN_MAX * kBM * 2);
+          // Cin rows n0.. (output columns), columns m0.. (output rows); box {128, BN}
+          tma_load_2d(&tm.m[t.prob][2], &ct_full[cb], sCt + cb * BN_MAX * kBM, m0, t.n_blk * p.bn, kEvictFirst);
+        }
+        __syncwarp();
+        ++it_p;
+      }
       const int cw = p.b_swz >> 1;   // MN-major B chunk width (elements)
       const int cb = p.b_swz * kBK;  // MN-major B chunk bytes (64 K-rows)
       for (int i = 0; i < nkb; ++i) {
@@ -414,10 +441,39 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
         for (int e = 0; e < 32; ++e)
           cin[e] = (row < p.M && n0 + 8 * e < p.N) ? __ldg(reinterpret_cast<const uint4*>(src) + e) : make_uint4(0, 0, 0, 0);
       }
+      if constexpr (EPI == 2) mbar_wait(&ct_full[acc], acc_phase);  // Cin block of this tile landed
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN_MAX;
       if (g.dbg == 4) {
+      } else if (EPI == 2) {
+        const int lr = q * 32 + lane;  // local output row
+#pragma unroll 1
+        for (int c = 0; c < p.bn; c += 32) {
+          if (n0 + c >= p.N) break;  // warp-uniform
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_row + c, v);
+          tmem_ld_wait();
+          if (row < p.M) {
+            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.D) + (long long)row * p.ldd + n0 + c;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              if (n0 + c + 8 * e < p.N) {
+                float f[8];
+#pragma unroll
+                for (int x = 0; x < 8; ++x)
+                  f[x] = __uint_as_float(v[8 * e + x]) +
+                         __bfloat162float(sCt[acc * BN_MAX * kBM + (c + 8 * e + x) * kBM + lr]);
+                uint4 o;
+                o.x = pack_bf16x2(f[0], f[1]);
+                o.y = pack_bf16x2(f[2], f[3]);
+                o.z = pack_bf16x2(f[4], f[5]);
+                o.w = pack_bf16x2(f[6], f[7]);
+                *reinterpret_cast<uint4*>(dst + 8 * e) = o;
+              }
+            }
+          }
+        }
       } else if (add256) {
 #pragma unroll
         for (int c8 = 0; c8 < 8; ++c8) {
@@ -470,6 +526,9 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote<CG>(&tempty[acc], 0);  // leader's barrier
+      if constexpr (EPI == 2) {
+        if (lane == 0) mbar_arrive(&ct_empty[acc]);  // Cin block buffer free
+      }
       if (p.counters) splitk_fixup(p, t, m0, n0, row, s_flag);
     }
   }
