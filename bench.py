@@ -285,6 +285,33 @@ def main():
             "frac": achieved / peaks["bf16_tflops"] if achieved else None, "traffic": traffic,
             "kernel": "gemm_main (tcgen05 Y / dX GEMM)", "peak_source": f"{peak_src} bf16 burst (cuBLAS 8192^3)",
             "flops_per_launch": flops_per_launch}
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            nl = json.load(f).get("gemm_main", {}).get("launches", [])
+        if nl:
+            roof["tensor_pipe_pct_ncu"] = sum(x.get("tensor_pipe_pct", 0) for x in nl) / len(nl)
+    except Exception:
+        pass
+    # HBM-bound rank-r kernels: algorithmic bytes per launch / live duration vs measured HBM
+    # copy bandwidth (SURVEY §8(d) "Algorithmic HBM bytes for the rank-r kernels").
+    hbm = peaks["hbm_gbs"]
+    alg = {
+        "gemm_proj": (2 * n * (k if fwd == 1 else 0) + 2 * n * r + 2 * k * r,  # forward1: Z2 = X·A
+                      2 * n * (k + m) + 4 * n * r + 2 * r * (k + m)),          # backward: Z1, Z2
+        "gemm_tokred": (2 * n * (k + m) + 4 * n * r,),                          # dA, dBᵀ partials
+        "gemm_wprime": (4 * k * m + 2 * r * (k + m),) * 2,
+    }
+    hbm_roof = {}
+    for nm, (cnt, ms_tot) in prof.items():
+        if nm not in alg or not cnt:
+            continue
+        per_step = cnt / args.steps
+        bytes_step = sum(alg[nm][: int(round(per_step))]) if nm == "gemm_proj" and fwd == 1 else \
+            alg[nm][-1] * per_step
+        gbs = bytes_step / (ms_tot / args.steps * 1e-3) / 1e9
+        hbm_roof[nm] = {"bound": "hbm", "bytes_per_step": bytes_step, "achieved": gbs, "peak": hbm,
+                        "unit": "GB/s", "frac": gbs / hbm}
+    roof["hbm_kernels"] = hbm_roof
 
     # ---------------- end to end through the C ABI with host buffers
     hx = ops["X"].pin_memory()

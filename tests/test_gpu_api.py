@@ -1,0 +1,127 @@
+"""GPU tests of the rest of the public surface: the time/hybrid selector, the autograd
+op, the host-buffer end-to-end step, and the tracing hooks — all through the C ABI and
+checked against the CPU fp64 oracle where they produce numbers."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+@pytest.fixture(scope="module")
+def rl():
+    from paper_2312_03415_b200 import runlora
+    return runlora
+
+
+def _np(t):
+    return t.detach().to(torch.float64).cpu().numpy()
+
+
+def _setup(rl, c):
+    ops = synth.operands(c)
+    d = {k: v.cuda() for k, v in ops.items()}
+    shape = rl.make_shape(c.n, c.k, c.m, c.r, c.torch_dtype)
+    out = {"Y": torch.empty(c.n, c.m, dtype=c.torch_dtype, device="cuda"),
+           "dX": torch.empty(c.n, c.k, dtype=c.torch_dtype, device="cuda"),
+           "dA": torch.empty(c.k, c.r, device="cuda"), "dB": torch.empty(c.r, c.m, device="cuda")}
+    return ops, d, shape, out
+
+
+@pytest.mark.parametrize("crit", ["time", "hybrid"])
+def test_selector_time_and_hybrid(rl, crit):
+    c = synth.case("sel", 0, 20, 2048, 1024, 1024, 16, "bf16")
+    ops, d, shape, out = _setup(rl, c)
+    h = rl.Handle(0)  # fresh handle: empty plan cache
+    criterion = rl.BY_TIME if crit == "time" else rl.HYBRID
+    p = h.select(shape, criterion, ops=dict(d, **out), grad_dtype=rl.F32)
+    pd = p.as_dict()
+    assert p.fwd in (1, 2) and 1 <= p.bwd <= 5
+    assert (p.flops_fwd_pick, p.flops_bwd_pick) == O.select_by_flops(c.n, c.k, c.m, c.r)
+    fmin = min(O.flops_backward(v, c.n, c.k, c.m, c.r) for v in range(1, 6))
+    for v in range(1, 6):
+        t = pd["time_bwd_us"][v]
+        if crit == "hybrid" and O.flops_backward(v, c.n, c.k, c.m, c.r) > 2 * fmin:
+            assert t is None  # not timed: more than 2x the FLOP minimum
+        else:
+            assert t is not None and t > 0
+    assert pd["time_fwd_us"][p.fwd] == min(t for t in pd["time_fwd_us"].values() if t is not None)
+    assert pd["time_bwd_us"][p.bwd] == min(t for t in pd["time_bwd_us"].values() if t is not None)
+    # cached: a second call returns the same plan without timing again
+    p2 = h.select(shape, criterion, ops=dict(d, **out), grad_dtype=rl.F32)
+    assert (p2.fwd, p2.bwd) == (p.fwd, p.bwd) and p2.time_bwd_us[p.bwd] == p.time_bwd_us[p.bwd]
+
+
+@pytest.mark.parametrize("plan", [(1, 1), (2, 5), (2, 4)])
+def test_autograd_function(rl, plan):
+    from paper_2312_03415_b200.lora import LoRALinearFunction
+    c = synth.case("ag", 0, 21, 384, 512, 256, 16, "bf16")
+    ops = synth.operands(c)
+    X = ops["X"].cuda().requires_grad_(True)
+    W = ops["W"].cuda()
+    A = ops["A"].cuda().requires_grad_(True)
+    B = ops["B"].cuda().requires_grad_(True)
+    Y = LoRALinearFunction.apply(X, W, A, B, *plan)
+    Y.backward(ops["dY"].cuda())
+    Xn, Wn, An, Bn, dYn = (_np(ops[k]) for k in ("X", "W", "A", "B", "dY"))
+    wA, wB, wX = O.reference_backward(Xn, Wn, An, Bn, dYn)
+    assert O.rel_fro(_np(Y), O.forward(1, Xn, Wn, An, Bn)) <= TOL
+    assert O.rel_fro(_np(X.grad), wX) <= TOL
+    assert O.rel_fro(_np(A.grad), wA) <= TOL
+    assert O.rel_fro(_np(B.grad), wB) <= TOL
+
+
+def test_step_host_end_to_end(rl):
+    c = synth.case("e2e", 0, 22, 1000, 1024, 768, 8, "bf16")
+    ops, d, shape, out = _setup(rl, c)
+    h = rl.handle(0)
+    host = {"X": ops["X"].pin_memory(), "dY": ops["dY"].pin_memory(),
+            "dA": torch.empty(c.k, c.r).pin_memory(), "dB": torch.empty(c.r, c.m).pin_memory(),
+            "Y": torch.empty(c.n, c.m, dtype=torch.bfloat16).pin_memory()}
+    dev = {"W": d["W"], "A": d["A"], "B": d["B"], "X": torch.empty_like(d["X"]), "dY": torch.empty_like(d["dY"]),
+           **out}
+    h.step_host(shape, 1, 1, host, dev, rl.F32)
+    torch.cuda.synchronize()
+    Xn, Wn, An, Bn, dYn = (_np(ops[k]) for k in ("X", "W", "A", "B", "dY"))
+    wA, wB, _ = O.reference_backward(Xn, Wn, An, Bn, dYn)
+    assert O.rel_fro(host["dA"].double().numpy(), wA) <= TOL
+    assert O.rel_fro(host["dB"].double().numpy(), wB) <= TOL
+    assert O.rel_fro(_np(host["Y"]), O.forward(1, Xn, Wn, An, Bn)) <= TOL
+
+
+def test_profiling_and_launch_count(rl):
+    c = synth.case("prof", 0, 23, 512, 512, 512, 16, "bf16")
+    ops, d, shape, out = _setup(rl, c)
+    h = rl.Handle(0)
+    l0 = h.launch_count()
+    h.profile_enable(True)
+    h.forward(1, shape, d["X"], d["W"], d["A"], d["B"], out["Y"])
+    h.backward(1, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], out["dX"], out["dA"], out["dB"])
+    torch.cuda.synchronize()
+    prof = h.profile_read(reset=True)
+    h.profile_enable(False)
+    launches = h.launch_count() - l0
+    assert launches == sum(v[0] for v in prof.values())
+    assert prof["gemm_main"][0] == 2 and all(v[1] > 0 for v in prof.values())
+    assert h.profile_read() == {}
+
+
+def test_fp32_c1_selected_pair_through_autograd(rl):
+    from paper_2312_03415_b200.lora import lora_linear
+    c = synth.C1
+    ops = synth.operands(c)
+    X = ops["X"].cuda().requires_grad_(True)
+    A = ops["A"].cuda().requires_grad_(True)
+    B = ops["B"].cuda().requires_grad_(True)
+    Y = lora_linear(X, ops["W"].cuda(), A, B)
+    Y.backward(ops["dY"].cuda())
+    Xn, Wn, An, Bn, dYn = (_np(ops[k]) for k in ("X", "W", "A", "B", "dY"))
+    wA, wB, wX = O.reference_backward(Xn, Wn, An, Bn, dYn)
+    for g, w in ((A.grad, wA), (B.grad, wB), (X.grad, wX)):
+        assert O.rel_fro(_np(g), w) <= 1e-5
