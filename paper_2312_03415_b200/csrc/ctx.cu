@@ -22,7 +22,6 @@ Ctx::Ctx(int device) : device_(device) {
     encode_fn_ = fn;
   if (const char* e = getenv("RUNLORA_MAIN_CG")) main_cg_ = atoi(e) == 1 ? 1 : 2;
   if (const char* e = getenv("RUNLORA_SPLITK_FIXUP")) fixup_ = atoi(e) != 0;
-  if (const char* e = getenv("RUNLORA_ROTATE_K")) rotate_k_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_OCC2")) occ2_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_PDL")) pdl_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_WPRIME_T")) wprime_t_ = atoi(e) != 0;

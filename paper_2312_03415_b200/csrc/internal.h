@@ -52,7 +52,6 @@ struct GemmReq {
   int splits;        // >= 1 (only with OUT_F32)
   int kb_per_split;
   bool a_stream_once;  // A operand is read once (evict-first hint)
-  bool rotate_k;       // per-unit rotated K walk (HBM-bound skinny products)
   int cg;              // 1: one CTA per 128-row tile; 2: CTA pair (cta_group::2) per 256-row tile
   KernelId kid;
   // in-kernel deterministic split-K fix-up (OUT_F32 + splits): see Prob in tc_gemm.cuh
@@ -74,7 +73,6 @@ class Ctx {
   static constexpr int kCounterCap = 1 << 16;
   int* counters() const { return counters_; }
   bool fixup_enabled() const { return counters_ != nullptr && fixup_; }
-  bool rotate_k() const { return rotate_k_; }
   bool occ2() const { return occ2_; }
   bool pdl() const { return pdl_; }
   bool wprime_t() const { return wprime_t_; }  // forward2 builds W'ᵀ (env RUNLORA_WPRIME_T=0 disables)    // programmatic dependent launch (env RUNLORA_PDL=0 disables)  // 2 CTAs/SM for rank-r kernels (env RUNLORA_OCC2=0 disables)
@@ -109,7 +107,6 @@ class Ctx {
   cudaStream_t side_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   bool fixup_ = false;     // env RUNLORA_SPLITK_FIXUP=1: in-kernel fix-up instead of the reducer launch
-  bool rotate_k_ = false;  // env RUNLORA_ROTATE_K=1: rotated K walks (measured slower on C2)
   bool occ2_ = true;
   bool pdl_ = true;
   bool wprime_t_ = true;

@@ -276,7 +276,8 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
     p.b_mn = r.b_mn;
     p.b_swz = b_swz;
     p.a_3d = a3 ? 1 : 0;
-    p.rotate = r.rotate_k ? 1 : 0;
+    static const bool snake = getenv("RUNLORA_SNAKE") == nullptr || atoi(getenv("RUNLORA_SNAKE")) != 0;
+    p.snake = (snake && r.splits <= 1 && r.kid == KID_GEMM_MAIN) ? 1 : 0;
     // all of B (N x K bf16) above ~48 MB -> banded raster (see decode_unit)
     const double b_bytes = 2.0 * (double)r.N * (double)(r.K1 + r.K2);
     p.raster_g = b_bytes > 48e6 ? 8 : 1;

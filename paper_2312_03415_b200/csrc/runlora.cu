@@ -233,7 +233,6 @@ runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, KernelI
     q[i].K1 = (int)j.K;
     q[i].BN = p.BN[i];
     q[i].a_stream_once = true;
-    q[i].rotate_k = c.rotate_k();
     float* Pi = reinterpret_cast<float*>(reinterpret_cast<char*>(P) + p.p_off[i]);
     if (p.direct) {
       q[i].out_mode = OUT_BF16;

@@ -50,7 +50,7 @@ struct Prob {
   int a_mn, b_mn;        // operand majorness (0 = K-major)
   int b_swz;             // MN-major B swizzle width in bytes (32, 64, 128); K-major operands use 128
   int a_3d, b_3d;        // MN-major operand loaded by one 3-D TMA box (all swizzle chunks at once)
-  int rotate;            // start each unit's K walk at a unit-dependent block (see producer)
+  int snake;             // alternate the K direction between a CTA's consecutive units (L2 reuse)
   int raster_g;          // output tiles are visited in bands of raster_g row tiles (1: row-major)
   int out_mode;          // OutMode
   uint32_t idesc;        // tcgen05 instruction descriptor
@@ -316,7 +316,9 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       const int kb1 = min(p.nk1, kb0 + p.kb_per_split);
       const int nmain = kb1 - kb0;
       const int nkb = nmain + (t.split == 0 ? p.nk2 : 0);
-      const int rot = nmain > 1 ? (int)(((unsigned)u * 7919u) % (unsigned)nmain) : 0;
+      // snake: every other round of this CTA walks K backwards, starting where the data it
+      // (and its neighbours) just streamed is still in L2
+      const bool rev = p.snake && (((u - group) / ngroups) & 1);
       if (g.dbg == 1 || g.dbg >= 3) continue;
       if constexpr (EPI == 2) {
         const int cb = it_p & 1;
@@ -341,10 +343,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
           const bool tail = i >= nmain;
           const CUtensorMap* ta = &tm.m[t.prob][tail ? 2 : 0];
           const CUtensorMap* tb = &tm.m[t.prob][tail ? 3 : 1];
-          // p.rotate: each unit starts its K walk at a different block so that concurrently
-          // running CTAs do not all hit the same column offset of their rows (DRAM channel
-          // camping on streams with power-of-two row pitch)
-          const int ki = (p.rotate && nmain > 1) ? (i + rot) % nmain : i;
+          const int ki = rev ? nmain - 1 - i : i;
           const int kc = (tail ? (i - nmain) : (kb0 + ki)) * kBK;
           if (!p.a_mn) {
             tma_load_2d<CG>(ta, fb, a, kc, m0, p.hint_a);
@@ -383,7 +382,9 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       const int kb1 = min(p.nk1, kb0 + p.kb_per_split);
       const int nmain = kb1 - kb0;
       const int nkb = nmain + (t.split == 0 ? p.nk2 : 0);
-      const int rot = nmain > 1 ? (int)(((unsigned)u * 7919u) % (unsigned)nmain) : 0;
+      // snake: every other round of this CTA walks K backwards, starting where the data it
+      // (and its neighbours) just streamed is still in L2
+      const bool rev = p.snake && (((u - group) / ngroups) & 1);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -397,7 +398,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       for (int i = 0; i < nkb; ++i) {
         if (g.dbg != 1 && g.dbg < 3) mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const int ki = (p.rotate && nmain > 1) ? (i + rot) % nmain : i;
+        const int ki = rev ? nmain - 1 - i : i;
         const int kleft = (i < nmain) ? (p.k1 - (kb0 + ki) * kBK) : (p.k2 - (i - nmain) * kBK);
         const int ksteps = min(kBK / 16, (kleft + 15) >> 4);
         const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
