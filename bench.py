@@ -138,34 +138,38 @@ def run_reference(args):
     return 0
 
 
-def cpu_baseline(c, fwd, bwd, target_s=12.0):
-    """The oracle timed on the host cores on a bounded sample (rank 0, N=1 only)."""
+def cpu_baseline(c, fwd, bwd, target_s=12.0, slice_tokens=1024):
+    """The oracle timed on the host cores on a bounded sample (rank 0, N=1 only): the
+    selected pair on consecutive 1024-token slices of the workload (cycling), until
+    ~target_s seconds of CPU work have been timed."""
     import oracle as O
-    ns = 256
-    ops = synth.operands(synth.case(c.name, c.cfg, c.sub, 4096, c.k, c.m, c.r, c.dtype))
+    ns = min(slice_tokens, c.n)
+    nslices = max(1, min(c.n, 4 * ns) // ns)
+    ops = synth.operands(synth.case(c.name, c.cfg, c.sub, nslices * ns, c.k, c.m, c.r, c.dtype))
     W, A, B = (ops[k].double().numpy() for k in ("W", "A", "B"))
     Xa, dYa = ops["X"].double().numpy(), ops["dY"].double().numpy()
-    t_total, tok_total = 0.0, 0
-    while t_total < target_s and ns <= 4096:
-        X, dY = Xa[:ns], dYa[:ns]
+    t_total, tok_total, i = 0.0, 0, 0
+    while t_total < target_s:
+        s0 = (i % nslices) * ns
+        X, dY = Xa[s0:s0 + ns], dYa[s0:s0 + ns]
         t0 = time.perf_counter()
         O.forward(fwd, X, W, A, B)
         O.backward(bwd, X, W, A, B, dY)
         t_total += time.perf_counter() - t0
         tok_total += ns
-        ns *= 2
+        i += 1
     return {"value": tok_total / t_total, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
-            "sample": f"contiguous token slices of {c.name} (256, 512, ... tokens, {tok_total} in total, "
-                      f"{t_total:.1f} s); oracle forward{fwd}+backward{bwd}, fp64 numpy/BLAS, includes the "
-                      "n-independent W+AB term per slice"}
+            "sample": f"{i} contiguous {ns}-token slices of {c.name} ({tok_total} tokens, {t_total:.1f} s of CPU "
+                      f"work); oracle forward{fwd}+backward{bwd}, fp64 numpy/BLAS on all host cores, each slice "
+                      "including the n-independent W+AB term"}
 
 
 # ------------------------------------------------------------------ main arm
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--r", type=int, default=16, choices=sorted(synth.C2))
     ap.add_argument("--impl", default="runlora", choices=["runlora", "reference"])
     ap.add_argument("--criterion", default="time", choices=["flops", "time", "hybrid"])
@@ -173,6 +177,8 @@ def main():
     ap.add_argument("--plan", default=None, help="force a variant pair, e.g. 1,1 (skips selection)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-default-chain", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only to exercise the multi-rank code path on one GPU (not a performance mode)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -186,10 +192,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     c = _case(args.r)
     n, k, m, r = c.n, c.k, c.m, c.r
     ops = synth.operands(c)
