@@ -25,6 +25,7 @@ Ctx::Ctx(int device) : device_(device) {
   if (const char* e = getenv("RUNLORA_OCC2")) occ2_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_PDL")) pdl_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_WPRIME_T")) wprime_t_ = atoi(e) != 0;
+  if (const char* e = getenv("RUNLORA_FUSED_GRADS")) fused_grads_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_L2PROMO_MN")) promo_mn_ = (CUtensorMapL2promotion)atoi(e);
   int prev = -1;
   cudaGetDevice(&prev);

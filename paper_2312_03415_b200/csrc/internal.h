@@ -24,6 +24,7 @@ enum KernelId : int {
   KID_GEMM_SMALL,      // Z2'·Bᵀ, Z2'ᵀ·A (backward3/4 adapter grads)
   KID_SPLITK_REDUCE,   // fixed-order split-K reduction / cast / transpose
   KID_SGEMM_F32,       // fp32 SIMT GEMM (RUNLORA_F32 path)
+  KID_GEMM_GRADS,      // fused Z1, Z2 -> dA, dB partials (backward1/5, one launch)
   KID_COUNT
 };
 extern const char* const kKernelNames[KID_COUNT];
@@ -60,6 +61,10 @@ struct GemmReq {
   void* fix_out;
   int64_t fix_ldo;
   int fix_bf16, fix_transpose, fix_accumulate;
+  // dataflow flags between problems of one launch (see Prob in tc_gemm.cuh)
+  int* dep_flags;
+  int* pub_flags;
+  unsigned epoch;
 };
 
 class Ctx {
@@ -81,6 +86,10 @@ class Ctx {
   cudaEvent_t fork_event();
   cudaEvent_t join_event();
   bool join_pending = false;
+  // fused adapter-gradient pass: per-128-row-tile flags (upper half of the counter array)
+  int* flags() const { return counters_ ? counters_ + kCounterCap / 2 : nullptr; }
+  unsigned next_epoch() { return ++epoch_; }
+  bool fused_grads() const { return fused_grads_; }
 
   // Encodes (or fetches from cache) a 2-D bf16 TMA descriptor with swz_bytes swizzle
   // (32, 64, 128): dims {cols, rows}, row stride ld*2 bytes, box {swz_bytes/2, box_rows}.
@@ -104,6 +113,8 @@ class Ctx {
   int num_sms_ = 148;
   int main_cg_ = 2;
   int* counters_ = nullptr;
+  unsigned epoch_ = 0;
+  bool fused_grads_ = true;
   cudaStream_t side_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   bool fixup_ = false;     // env RUNLORA_SPLITK_FIXUP=1: in-kernel fix-up instead of the reducer launch

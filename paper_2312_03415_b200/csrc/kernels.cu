@@ -13,7 +13,7 @@ namespace runlora {
 
 const char* const kKernelNames[KID_COUNT] = {
     "gemm_main",      "gemm_wprime", "gemm_proj",        "gemm_tokred",
-    "gemm_dense_xtdy", "gemm_small",  "splitk_reduce", "sgemm_f32",
+    "gemm_dense_xtdy", "gemm_small",  "splitk_reduce", "sgemm_f32", "gemm_grads_fused",
 };
 
 namespace {
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(256) sgemm_kernel(int M, int N, int K, const f
 }  // namespace
 
 cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t s, std::string* err) {
-  if (nreq < 1 || nreq > 2) return cudaErrorInvalidValue;
+  if (nreq < 1 || nreq > kMaxProb) return cudaErrorInvalidValue;
   Tmaps tm;
   GemmArgs g;
   memset(&g, 0, sizeof g);
@@ -297,6 +297,9 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
     p.fix_bf16 = r.fix_bf16;
     p.fix_transpose = r.fix_transpose;
     p.fix_accumulate = r.fix_accumulate;
+    p.dep_flags = r.dep_flags;
+    p.pub_flags = r.pub_flags;
+    p.epoch = r.epoch;
     p.hint_a = r.a_stream_once ? kEvictFirst : kEvictNormal;
     p.hint_b = kEvictLast;
     g.total_units += p.units;
@@ -304,7 +307,7 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
   }
   g.nprob = nreq;
   if (const char* d = getenv("RUNLORA_DBG_GEMM")) g.dbg = atoi(d);
-  if (nreq == 1) g.p[1] = g.p[0], g.p[1].units = 0;
+  for (int q = nreq; q < kMaxProb; ++q) g.p[q] = g.p[0], g.p[q].units = 0;
   if (g.total_units <= 0) return cudaSuccess;
   ctx.launch_begin(s, reqs[0].kid);
   cudaError_t e = dispatch_tc(ctx, bn_max, cg, ctx.occ2() && reqs[0].a_stream_once, tm, g, s);

@@ -46,11 +46,16 @@ runlora_status_t fail(runlora_status_t st, const std::string& msg) {
     if (_st != RUNLORA_OK) return _st;     \
   } while (0)
 
+// Makes the handle's device (and its primary context) current on the calling thread —
+// callers such as PyTorch's autograd engine run the backward on their own threads, where
+// the driver-API TMA encoder would otherwise see no current context — and restores the
+// previously selected device afterwards.
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
-    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
-    else prev = -1;
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    cudaSetDevice(dev);
+    if (prev == dev) prev = -1;
   }
   ~DeviceGuard() {
     if (prev >= 0) cudaSetDevice(prev);
@@ -441,11 +446,95 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
   return gemm(c, q, st);
 }
 
+// backward1/5 adapter gradients in ONE launch: the Z1 = dY·Bᵀ and Z2 = X·A tiles are
+// scheduled first and publish a per-128-token flag; the dA = Xᵀ·Z1 / dBᵀ = dYᵀ·Z2 split-K
+// units of the same persistent launch wait only for the Z rows of their own token range.
+// Returns false (nothing launched) when the projections would not write bf16 directly.
+bool fused_grads_bf16(Ctx& c, const runlora_shape_t& s, const void* X, const void* A, const void* B, const void* dY,
+                      void* dA, void* dB, bool gb, bool acc, Bufs& b, cudaStream_t st, bool defer,
+                      runlora_status_t* status) {
+  Skinny pj[2] = {job_Z1(s, dY, B, b.z1), job_Z2(s, X, A, b.z2)};
+  Skinny tj[2] = {job_dA_tok(s, X, b.z1, dA, gb, acc), job_dB_tok(s, dY, b.z2, dB, gb, acc)};
+  const SkinnyPlan pp = plan_skinny(pj, 2);
+  const SkinnyPlan tp = plan_skinny(tj, 2);
+  const int64_t mt = (s.n + kBM - 1) / kBM;
+  if (!c.fused_grads() || !c.flags() || !pp.direct || tp.direct || 2 * mt > Ctx::kCounterCap / 2) return false;
+  const unsigned epoch = c.next_epoch();
+  int* f1 = c.flags();
+  int* f2 = f1 + mt;
+  GemmReq q[4];
+  ReduceJob rj[2];
+  for (int i = 0; i < 2; ++i) {
+    const Skinny& j = pj[i];
+    q[i] = base_req((int)j.rows, (int)j.r, KID_GEMM_GRADS);
+    q[i].a = j.a;
+    q[i].a_mn = j.a_mn;
+    q[i].b = j.b;
+    q[i].b_mn = j.b_mn;
+    q[i].K1 = (int)j.K;
+    q[i].BN = pp.BN[i];
+    q[i].a_stream_once = true;
+    q[i].out_mode = OUT_BF16;
+    q[i].D = j.out;
+    q[i].ldd = j.ldo;
+    q[i].pub_flags = i == 0 ? f1 : f2;
+    q[i].epoch = epoch;
+  }
+  for (int i = 0; i < 2; ++i) {
+    const Skinny& j = tj[i];
+    GemmReq& r = q[2 + i];
+    r = base_req((int)j.rows, tp.Npad[i], KID_GEMM_TOKRED);
+    r.a = j.a;
+    r.a_mn = j.a_mn;
+    r.b = j.b;
+    r.b_mn = j.b_mn;
+    r.K1 = (int)j.K;
+    r.BN = tp.BN[i];
+    r.a_stream_once = true;
+    float* Pi = reinterpret_cast<float*>(reinterpret_cast<char*>(b.P) + tp.p_off[i]);
+    r.out_mode = OUT_F32;
+    r.D = Pi;
+    r.ldd = tp.Npad[i];
+    r.split_stride = j.rows * (int64_t)tp.Npad[i];
+    r.splits = tp.splits[i];
+    r.kb_per_split = tp.kps[i];
+    r.dep_flags = i == 0 ? f1 : f2;
+    r.epoch = epoch;
+    rj[i] = ReduceJob{Pi, tp.splits[i], r.split_stride, (int)j.rows, (int)j.r, tp.Npad[i], j.out, j.out_bf16 ? 1 : 0,
+                      j.ldo, j.transpose ? 1 : 0, j.accumulate ? 1 : 0};
+  }
+  std::string err;
+  cudaError_t e = launch_tc_gemm(c, q, 4, st, &err);
+  if (e != cudaSuccess) {
+    *status = fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
+    return true;
+  }
+  cudaStream_t rs = st;
+  if (defer) {
+    rs = c.side_stream();
+    cudaEventRecord(c.fork_event(), st);
+    cudaStreamWaitEvent(rs, c.fork_event(), 0);
+  }
+  e = launch_splitk_reduce(c, rj, 2, rs);
+  if (e != cudaSuccess) {
+    *status = cuda_fail(e, "splitk_reduce launch");
+    return true;
+  }
+  if (defer) {
+    cudaEventRecord(c.join_event(), rs);
+    c.join_pending = true;
+  }
+  *status = RUNLORA_OK;
+  return true;
+}
+
 runlora_status_t params_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* X, const void* A, const void* B,
                              const void* dY, void* dA, void* dB, bool gb, bool acc, Bufs& b, cudaStream_t st,
                              bool defer = false) {
   const int64_t n = s.n, k = s.k, m = s.m;
   if (v == 1 || v == 5) {  // Alg. 1 / Alg. 5: Z1, Z2 | dA = Xᵀ·Z1, dB = Z2ᵀ·dY
+    runlora_status_t fst;
+    if (fused_grads_bf16(c, s, X, A, B, dY, dA, dB, gb, acc, b, st, defer, &fst)) return fst;
     Skinny pj[2] = {job_Z1(s, dY, B, b.z1), job_Z2(s, X, A, b.z2)};
     RL_TRY(run_skinny(c, pj, 2, b.P, KID_GEMM_PROJ, st));
     Skinny tj[2] = {job_dA_tok(s, X, b.z1, dA, gb, acc), job_dB_tok(s, dY, b.z2, dB, gb, acc)};

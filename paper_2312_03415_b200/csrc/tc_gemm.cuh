@@ -69,17 +69,26 @@ struct Prob {
   void* fix_out;
   long long fix_ldo;
   int fix_bf16, fix_transpose, fix_accumulate;
+  // Dataflow between problems of one launch (fused adapter-gradient pass): a unit of this
+  // problem covering K rows [kb0*64, kb1*64) first waits until dep_flags[t] == epoch for
+  // every 128-row tile t of the problem that produces its B operand; a problem with
+  // pub_flags publishes pub_flags[m_blk] = epoch once its tile's rows are stored.
+  int* dep_flags;
+  int* pub_flags;
+  unsigned epoch;
 };
 
+constexpr int kMaxProb = 4;
+
 struct GemmArgs {
-  Prob p[2];
+  Prob p[kMaxProb];
   int nprob;
   int total_units;
   int dbg;  // 0 normal; 1: no TMA (MMA-only); 2: no MMA (TMA-only); 3: as 1 + no stores; 4: as 1 + no epilogue
 };
 
 struct Tmaps {  // per problem: A1, B1, A2, B2
-  CUtensorMap m[2][4];
+  CUtensorMap m[kMaxProb][4];
 };
 
 constexpr int kBM = 128;  // rows per CTA
@@ -108,9 +117,9 @@ struct Unit {
 __device__ __forceinline__ Unit decode_unit(const GemmArgs& g, int u) {
   Unit t;
   t.prob = 0;
-  if (u >= g.p[0].units) {
-    u -= g.p[0].units;
-    t.prob = 1;
+  while (t.prob < kMaxProb - 1 && u >= g.p[t.prob].units) {
+    u -= g.p[t.prob].units;
+    ++t.prob;
   }
   const Prob& p = g.p[t.prob];
   const int per_split = p.num_m_tiles * p.num_n_tiles;
@@ -331,6 +340,17 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
         __syncwarp();
         ++it_p;
       }
+      if (p.dep_flags) {
+        // wait for the producer problem's 128-row tiles covering this unit's K rows
+        if (lane == 0) {
+          const int t_lo = (kb0 * kBK) / kBM, t_hi = (kb1 * kBK + kBM - 1) / kBM;
+          for (int tt = t_lo; tt < t_hi; ++tt) {
+            while (ld_acquire_gpu(p.dep_flags + tt) != (int)p.epoch) __nanosleep(64);
+          }
+          fence_proxy_async_global();  // generic-proxy writes -> this thread's TMA reads
+        }
+        __syncwarp();
+      }
       const int cw = p.b_swz >> 1;   // MN-major B chunk width (elements)
       const int cb = p.b_swz * kBK;  // MN-major B chunk bytes (64 K-rows)
       for (int i = 0; i < nkb; ++i) {
@@ -531,6 +551,11 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
         if (lane == 0) mbar_arrive(&ct_empty[acc]);  // Cin block buffer free
       }
       if (p.counters) splitk_fixup(p, t, m0, n0, row, s_flag);
+      if (p.pub_flags) {  // this tile's rows are stored: publish for dependent problems
+        __threadfence();
+        epi_bar();
+        if (threadIdx.x == 4 * 32) st_release_gpu(p.pub_flags + t.m_blk, (int)p.epoch);
+      }
     }
   }
   tc_fence_before();
