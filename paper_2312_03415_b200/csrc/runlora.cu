@@ -861,47 +861,63 @@ runlora_status_t runlora_select(runlora_handle_t h, const runlora_shape_t* s, in
   cudaEvent_t e0, e1;
   if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
     return fail(RUNLORA_ERR_TIMING, "cudaEventCreate failed");
+  // Candidates are timed round-robin (one rep of each per round) so that clock and power
+  // drift under the 1 kW cap affects all of them alike; median of 15 rounds after 3.
   const int warm = 3, reps = 15;
-  auto time_it = [&](auto&& run, float* med) -> runlora_status_t {
-    std::vector<float> t;
-    for (int i = 0; i < warm + reps; ++i) {
-      cudaEventRecord(e0, st);
-      RL_TRY(run());
-      cudaEventRecord(e1, st);
-      if (cudaEventSynchronize(e1) != cudaSuccess) return fail(RUNLORA_ERR_TIMING, "event sync failed");
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, e0, e1);
-      if (i >= warm) t.push_back(ms * 1000.f);
-    }
-    *med = median(t);
-    return RUNLORA_OK;
-  };
   const uint64_t fmin = std::min(p.flops_fwd[1], p.flops_fwd[2]);
   uint64_t bmin = p.flops_bwd[1];
   for (int v = 2; v <= 5; ++v) bmin = std::min(bmin, p.flops_bwd[v]);
+  std::vector<int> cands;  // 1..2 forward, 11..15 backward
+  for (int v = 1; v <= 2; ++v)
+    if (!(criterion == RUNLORA_HYBRID && p.flops_fwd[v] > 2 * fmin)) cands.push_back(v);
+  for (int v = 1; v <= 5; ++v)
+    if (!(criterion == RUNLORA_HYBRID && p.flops_bwd[v] > 2 * bmin)) cands.push_back(10 + v);
+  std::vector<std::vector<float>> times(cands.size());
   runlora_status_t st_all = RUNLORA_OK;
-  for (int v = 1; v <= 2 && st_all == RUNLORA_OK; ++v) {
-    if (criterion == RUNLORA_HYBRID && p.flops_fwd[v] > 2 * fmin) continue;
-    st_all = time_it([&] { return do_forward(h, v, s, ops->X, ops->W, ops->A, ops->B, ops->Y, ws, ws_bytes, stream); },
-                     &p.time_fwd_us[v]);
-  }
-  for (int v = 1; v <= 5 && st_all == RUNLORA_OK; ++v) {
-    if (criterion == RUNLORA_HYBRID && p.flops_bwd[v] > 2 * bmin) continue;
-    st_all = time_it(
-        [&] {
-          return do_backward(h, v, s, ops->X, ops->W, ops->A, ops->B, ops->dY, ops->dX, ops->dA, ops->dB,
+  for (int i = 0; i < warm + reps && st_all == RUNLORA_OK; ++i) {
+    for (size_t ci = 0; ci < cands.size() && st_all == RUNLORA_OK; ++ci) {
+      const int v = cands[ci];
+      cudaEventRecord(e0, st);
+      if (v < 10)
+        st_all = do_forward(h, v, s, ops->X, ops->W, ops->A, ops->B, ops->Y, ws, ws_bytes, stream);
+      else
+        st_all = do_backward(h, v - 10, s, ops->X, ops->W, ops->A, ops->B, ops->dY, ops->dX, ops->dA, ops->dB,
                              ops->grad_dtype, 0, ws, ws_bytes, stream);
-        },
-        &p.time_bwd_us[v]);
+      cudaEventRecord(e1, st);
+      if (st_all != RUNLORA_OK) break;
+      if (cudaEventSynchronize(e1) != cudaSuccess) {
+        st_all = fail(RUNLORA_ERR_TIMING, "event sync failed");
+        break;
+      }
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (i >= warm) times[ci].push_back(ms * 1000.f);
+    }
+  }
+  if (st_all == RUNLORA_OK) {
+    for (size_t ci = 0; ci < cands.size(); ++ci) {
+      const int v = cands[ci];
+      if (v < 10) p.time_fwd_us[v] = median(times[ci]);
+      else p.time_bwd_us[v - 10] = median(times[ci]);
+    }
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (st_all != RUNLORA_OK) return st_all;
-  int bf = 0, bb = 0;
-  for (int v = 1; v <= 2; ++v)
-    if (!std::isnan(p.time_fwd_us[v]) && (bf == 0 || p.time_fwd_us[v] < p.time_fwd_us[bf])) bf = v;
-  for (int v = 1; v <= 5; ++v)
-    if (!std::isnan(p.time_bwd_us[v]) && (bb == 0 || p.time_bwd_us[v] < p.time_bwd_us[bb])) bb = v;
+  // argmin of the medians; candidates within 1 % of the fastest count as a tie (timer and
+  // clock noise) and the tie goes to fewer FLOPs, then the lower index (R9).
+  auto pick = [](const float* t, const uint64_t* fl, int lo, int hi) {
+    int best = 0;
+    for (int v = lo; v <= hi; ++v)
+      if (!std::isnan(t[v]) && (best == 0 || t[v] < t[best])) best = v;
+    if (best == 0) return 0;
+    int sel = best;
+    for (int v = lo; v <= hi; ++v)
+      if (!std::isnan(t[v]) && t[v] <= 1.01f * t[best] && (fl[v] < fl[sel] || (fl[v] == fl[sel] && v < sel))) sel = v;
+    return sel;
+  };
+  const int bf = pick(p.time_fwd_us, p.flops_fwd, 1, 2);
+  const int bb = pick(p.time_bwd_us, p.flops_bwd, 1, 5);
   if (bf == 0 || bb == 0) return fail(RUNLORA_ERR_TIMING, "no candidate could be timed");
   p.fwd = bf;
   p.bwd = bb;
