@@ -309,7 +309,6 @@ def main():
         "gemm_proj": (2 * n * (k if fwd == 1 else 0) + 2 * n * r + 2 * k * r,  # forward1: Z2 = X·A
                       2 * n * (k + m) + 4 * n * r + 2 * r * (k + m)),          # backward: Z1, Z2
         "gemm_tokred": (2 * n * (k + m) + 4 * n * r,),                          # dA, dBᵀ partials
-        "gemm_grads_fused": (4 * n * (k + m) + 8 * n * r + 2 * r * (k + m),),   # both, one launch
         "gemm_wprime": (4 * k * m + 2 * r * (k + m),) * 2,
     }
     hbm_roof = {}

@@ -25,6 +25,10 @@ extern "C" {
 runlora_status_t runlora_debug_gemm(runlora_handle_t h, int M, int N, int K1, const void* A1, int a_mn,
                                     const void* B1, int b_mn, int K2, const void* A2, const void* B2, int out_mode,
                                     void* D, const void* Cin, int BN, int splits, int cg, void* stream);
+/* Debug timeline of the last launch of kernel id RUNLORA_TRACE (env, read at handle creation):
+ * 8 uint64 per unit {producer start, dependencies met, last load issued, epilogue done (ns),
+ * CTA index, problem index}.  Returns the number of units copied (0 if tracing is off). */
+int runlora_debug_trace(runlora_handle_t h, unsigned long long* host, int max_units);
 #ifdef __cplusplus
 }
 #endif

@@ -24,8 +24,6 @@ Ctx::Ctx(int device) : device_(device) {
   if (const char* e = getenv("RUNLORA_SPLITK_FIXUP")) fixup_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_OCC2")) occ2_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_PDL")) pdl_ = atoi(e) != 0;
-  if (const char* e = getenv("RUNLORA_WPRIME_T")) wprime_t_ = atoi(e) != 0;
-  if (const char* e = getenv("RUNLORA_FUSED_GRADS")) fused_grads_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_L2PROMO_MN")) promo_mn_ = (CUtensorMapL2promotion)atoi(e);
   int prev = -1;
   cudaGetDevice(&prev);
@@ -38,6 +36,22 @@ Ctx::Ctx(int device) : device_(device) {
   } else {
     counters_ = nullptr;
   }
+  if (const char* e = getenv("RUNLORA_TMA_STORE_MAIN")) tma_store_main_ = atoi(e) != 0;
+  if (const char* e = getenv("RUNLORA_TMA_STORE_WPRIME")) tma_store_wprime_ = atoi(e) != 0;
+  if (const char* e = getenv("RUNLORA_TRACE")) {
+    trace_kid = atoi(e);
+    if (cudaMalloc(&trace, sizeof(unsigned long long) * 8 * kTraceUnits) != cudaSuccess) trace = nullptr;
+  }
+  {
+    std::vector<uint16_t> eye(128 * 128, 0);
+    for (int i = 0; i < 128; ++i) eye[i * 128 + i] = 0x3F80;  // bf16 1.0
+    if (cudaMalloc(&identity_, eye.size() * 2) != cudaSuccess ||
+        cudaMemcpy(identity_, eye.data(), eye.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess) {
+      if (identity_) cudaFree(identity_);
+  if (trace) cudaFree(trace);
+      identity_ = nullptr;
+    }
+  }
   if (prev >= 0) cudaSetDevice(prev);
 }
 
@@ -49,9 +63,12 @@ Ctx::~Ctx() {
   for (auto e : free_events_) cudaEventDestroy(e);
   if (cur_start_) cudaEventDestroy(cur_start_);
   if (counters_) cudaFree(counters_);
+  if (identity_) cudaFree(identity_);
+  if (trace) cudaFree(trace);
   if (side_) cudaStreamDestroy(side_);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
+  if (ev_arep_) cudaEventDestroy(ev_arep_);
 }
 
 cudaStream_t Ctx::side_stream() {
@@ -61,6 +78,10 @@ cudaStream_t Ctx::side_stream() {
 cudaEvent_t Ctx::fork_event() {
   if (!ev_fork_) cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming);
   return ev_fork_;
+}
+cudaEvent_t Ctx::arep_event() {
+  if (!ev_arep_) cudaEventCreateWithFlags(&ev_arep_, cudaEventDisableTiming);
+  return ev_arep_;
 }
 cudaEvent_t Ctx::join_event() {
   if (!ev_join_) cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming);

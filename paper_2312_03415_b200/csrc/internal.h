@@ -18,13 +18,13 @@ namespace runlora {
 enum KernelId : int {
   KID_GEMM_MAIN = 0,   // Y / dX GEMMs (dominant, tensor-bound)
   KID_GEMM_WPRIME,     // W + A·B (rank-r update, HBM-bound)
-  KID_GEMM_PROJ,       // X·A, dY·Bᵀ (rank-r projections, HBM-bound)
-  KID_GEMM_TOKRED,     // Xᵀ·Z1, dYᵀ·Z2 (token reductions, HBM-bound)
+  KID_GEMM_PROJ,       // X·A, dY·Bᵀ (rank-r projections, HBM-bound; K-split bf16 partials)
+  KID_GEMM_TOKRED,     // Xᵀ·Z1, dYᵀ·Z2 (token reductions, HBM-bound; folds Z's partials)
   KID_GEMM_DENSE_XTDY, // Xᵀ·dY (backward2..4 dense intermediate)
   KID_GEMM_SMALL,      // Z2'·Bᵀ, Z2'ᵀ·A (backward3/4 adapter grads)
   KID_SPLITK_REDUCE,   // fixed-order split-K reduction / cast / transpose
   KID_SGEMM_F32,       // fp32 SIMT GEMM (RUNLORA_F32 path)
-  KID_GEMM_GRADS,      // fused Z1, Z2 -> dA, dB partials (backward1/5, one launch)
+  KID_REPEAT_COLS,     // A repeated along its columns (dX tail against Z1's partial blocks)
   KID_COUNT
 };
 extern const char* const kKernelNames[KID_COUNT];
@@ -61,10 +61,10 @@ struct GemmReq {
   void* fix_out;
   int64_t fix_ldo;
   int fix_bf16, fix_transpose, fix_accumulate;
-  // dataflow flags between problems of one launch (see Prob in tc_gemm.cuh)
-  int* dep_flags;
-  int* pub_flags;
-  unsigned epoch;
+  int fold, fold_w;  // OUT_F32_FOLD
+  bool tail_diag;  // a2 = 128x128 identity, b2 read at the tile's own rows (see Prob)
+  int a_policy;      // L2 policy of the A operand: 0 from a_stream_once, 1 normal, 2 evict-first
+  bool tma_store;  // OUT_BF16 through the TMA-store epilogue (all problems of a launch alike)
 };
 
 class Ctx {
@@ -78,18 +78,22 @@ class Ctx {
   static constexpr int kCounterCap = 1 << 16;
   int* counters() const { return counters_; }
   bool fixup_enabled() const { return counters_ != nullptr && fixup_; }
-  bool occ2() const { return occ2_; }
-  bool pdl() const { return pdl_; }
-  bool wprime_t() const { return wprime_t_; }  // forward2 builds W'ᵀ (env RUNLORA_WPRIME_T=0 disables)    // programmatic dependent launch (env RUNLORA_PDL=0 disables)  // 2 CTAs/SM for rank-r kernels (env RUNLORA_OCC2=0 disables)
+  bool occ2() const { return occ2_; }  // 2 CTAs/SM for rank-r kernels (env RUNLORA_OCC2=0 disables)
+  bool pdl() const { return pdl_; }    // programmatic dependent launch (env RUNLORA_PDL=0 disables)
   // Side stream for small work that can overlap the next big GEMM (fork/join by events).
   cudaStream_t side_stream();
   cudaEvent_t fork_event();
   cudaEvent_t join_event();
+  cudaEvent_t arep_event();  // A repeated for backward1's dX tail is ready (side stream)
   bool join_pending = false;
-  // fused adapter-gradient pass: per-128-row-tile flags (upper half of the counter array)
-  int* flags() const { return counters_ ? counters_ + kCounterCap / 2 : nullptr; }
-  unsigned next_epoch() { return ++epoch_; }
-  bool fused_grads() const { return fused_grads_; }
+  // 128x128 bf16 identity (device): A operand of the block-diagonal tail that adds W in W + A·B
+  const void* identity() const { return identity_; }
+  // debug timeline buffer (env RUNLORA_TRACE=<kernel id>): see GemmArgs::trace
+  unsigned long long* trace = nullptr;
+  int trace_kid = -1;
+  static constexpr int kTraceUnits = 1 << 16;
+  bool tma_store_main() const { return tma_store_main_; }
+  bool tma_store_wprime() const { return tma_store_wprime_; }
 
   // Encodes (or fetches from cache) a 2-D bf16 TMA descriptor with swz_bytes swizzle
   // (32, 64, 128): dims {cols, rows}, row stride ld*2 bytes, box {swz_bytes/2, box_rows}.
@@ -113,14 +117,14 @@ class Ctx {
   int num_sms_ = 148;
   int main_cg_ = 2;
   int* counters_ = nullptr;
-  unsigned epoch_ = 0;
-  bool fused_grads_ = true;
+  void* identity_ = nullptr;
+  bool tma_store_main_ = false;   // env RUNLORA_TMA_STORE_MAIN=1
+  bool tma_store_wprime_ = true;  // env RUNLORA_TMA_STORE_WPRIME=0
   cudaStream_t side_ = nullptr;
-  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_arep_ = nullptr;
   bool fixup_ = false;     // env RUNLORA_SPLITK_FIXUP=1: in-kernel fix-up instead of the reducer launch
   bool occ2_ = true;
   bool pdl_ = true;
-  bool wprime_t_ = true;
   CUtensorMapL2promotion promo_mn_ = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;  // 3-D (MN-major) boxes       // env RUNLORA_OCC2=0: one CTA per SM for the rank-r kernels too
   void* encode_fn_ = nullptr;
   std::mutex tmap_mu_;
@@ -156,6 +160,8 @@ struct ReduceJob {
   int transpose, accumulate;
 };
 cudaError_t launch_splitk_reduce(Ctx& ctx, const ReduceJob* jobs, int njobs, cudaStream_t s);
+// dst[i, t*cols + j] = src[i, j] for t < reps (bf16, row-major; 16-byte column groups).
+cudaError_t launch_repeat_cols(Ctx& ctx, const void* src, int rows, int cols, int reps, void* dst, cudaStream_t s);
 // fp32 SIMT GEMM: C[i,j] = (acc ? C[i,j] : 0) + (Cadd ? Cadd[i,j] : 0) + sum_t A(i,t) B(t,j),
 // A(i,t) = A[i*sa0 + t*sa1], B(t,j) = B[t*sb0 + j*sb1].
 cudaError_t launch_sgemm(Ctx& ctx, int M, int N, int K, const float* A, int64_t sa0, int64_t sa1, const float* B,

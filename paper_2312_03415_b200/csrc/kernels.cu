@@ -2,6 +2,8 @@
 // fp32 SIMT GEMM.  See tc_gemm.cuh for the GEMM design.
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -13,7 +15,7 @@ namespace runlora {
 
 const char* const kKernelNames[KID_COUNT] = {
     "gemm_main",      "gemm_wprime", "gemm_proj",        "gemm_tokred",
-    "gemm_dense_xtdy", "gemm_small",  "splitk_reduce", "sgemm_f32", "gemm_grads_fused",
+    "gemm_dense_xtdy", "gemm_small",  "splitk_reduce", "sgemm_f32", "repeat_cols",
 };
 
 namespace {
@@ -37,13 +39,16 @@ cudaError_t launch_pdl(Ctx& ctx, void (*kern)(KArgs...), dim3 grid, dim3 block, 
 }
 
 template <int BN, int CG, int OCC = 1, int EPI = 0>
-cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, const GemmArgs& g, cudaStream_t s) {
+cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, GemmArgs& g, cudaStream_t s) {
   auto kern = tc_gemm_kernel<BN, CG, OCC, EPI>;
   constexpr uint32_t smem = TileCfg<BN, CG, OCC, EPI>::SMEM_BYTES;
   static bool attr_set[kMaxDevices] = {};
   const int dev = ctx.device();
   if (dev < kMaxDevices && !attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    // the whole unified L1/shared array as shared memory, so OCC = 2 CTAs are co-resident
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
   }
@@ -70,14 +75,24 @@ cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, const GemmArgs& g, cudaStream_t s)
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, kern, tm, g);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tm, g);
+  static const bool dbg_launch = getenv("RUNLORA_DEBUG_LAUNCH") != nullptr;
+  if (dbg_launch) {
+    int occ = -1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGemmThreads, smem);
+    fprintf(stderr, "[runlora] tc_gemm<%d,%d,%d,%d> grid %d smem %u occupancy/SM %d units %d: %s\n", BN, CG, OCC, EPI,
+            groups * CG, smem, occ, g.total_units, cudaGetErrorString(e));
+  }
+  return e;
 }
 
-cudaError_t dispatch_tc(Ctx& ctx, int bn_max, int cg, bool occ2, const Tmaps& tm, const GemmArgs& g,
+cudaError_t dispatch_tc(Ctx& ctx, int bn_max, int cg, bool occ2, bool tma_store, const Tmaps& tm, GemmArgs& g,
                         cudaStream_t s) {
-  if (cg == 1 && bn_max == 256 && g.p[0].out_mode == OUT_BF16_ADD) return run_tc<256, 1, 1, 1>(ctx, tm, g, s);
-  if (cg == 1 && bn_max == 256 && g.p[0].out_mode == OUT_BF16_ADD_T) return run_tc<256, 1, 1, 2>(ctx, tm, g, s);
-  if (g.p[0].out_mode == OUT_BF16_ADD || g.p[0].out_mode == OUT_BF16_ADD_T) return cudaErrorNotSupported;
+  if (tma_store) {
+    if (cg == 1 && bn_max == 256) return run_tc<256, 1, 1, 3>(ctx, tm, g, s);
+    if (cg == 2 && bn_max == 256) return run_tc<256, 2, 1, 3>(ctx, tm, g, s);
+    return cudaErrorNotSupported;
+  }
   if (cg == 2) {
     if (bn_max == 256) return run_tc<256, 2>(ctx, tm, g, s);
     if (bn_max == 128) return run_tc<128, 2>(ctx, tm, g, s);
@@ -160,6 +175,20 @@ __global__ void __launch_bounds__(256, 4) splitk_reduce_kernel(const __grid_cons
   }
 }
 
+// ------------------------------------------------------------ column repeat
+__global__ void __launch_bounds__(256) repeat_cols_kernel(const uint4* __restrict__ src, int rows, int g, int reps,
+                                                          uint4* __restrict__ dst) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const long long total = (long long)rows * g * reps;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long i = idx / ((long long)g * reps);
+    const int c = (int)(idx % g);
+    dst[idx] = src[i * g + c];
+  }
+}
+
 // ------------------------------------------------------------ fp32 SIMT GEMM
 // 64x64 output tile per 256-thread CTA, 4x4 per thread, K step 16; true FP32 FFMA.
 __global__ void __launch_bounds__(256) sgemm_kernel(int M, int N, int K, const float* __restrict__ A, long long sa0,
@@ -223,10 +252,15 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
   GemmArgs g;
   memset(&g, 0, sizeof g);
   const int cg = reqs[0].cg > 1 ? 2 : 1;
+  const bool tma_store = reqs[0].tma_store;
   int bn_max = 0;
   for (int q = 0; q < nreq; ++q) {
     const GemmReq& r = reqs[q];
-    if ((r.cg > 1 ? 2 : 1) != cg) return cudaErrorInvalidValue;
+    if ((r.cg > 1 ? 2 : 1) != cg || r.tma_store != tma_store) return cudaErrorInvalidValue;
+    if (r.tma_store && (r.out_mode != OUT_BF16 || r.BN != 256 || r.splits > 1)) {
+      if (err) *err = "tc_gemm: TMA-store epilogue needs a plain bf16 output with 256-wide tiles";
+      return cudaErrorInvalidValue;
+    }
     // MN-major B: 128B swizzle in 64-column chunks, or one 16/32-column chunk (32B/64B swizzle)
     const int nb = r.BN / cg;
     const int b_swz = !r.b_mn ? 128 : (nb % 64 == 0 ? 128 : nb == 32 ? 64 : nb == 16 ? 32 : 0);
@@ -253,11 +287,9 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
       tm.m[q][2] = tm.m[q][0];
       tm.m[q][3] = tm.m[q][1];
     }
-    if (r.out_mode == OUT_BF16_ADD_T) {
-      // Cin stored [N rows][M cols] (ld = ldc): one un-swizzled {128, BN} block per tile
-      if (r.K2 > 0 || r.BN != 256 || cg != 1) return cudaErrorNotSupported;
-      const DeviceMat cm{r.Cin, (int64_t)r.N, (int64_t)r.M, r.ldc};
-      if (!ctx.tmap(cm, 256, &tm.m[q][2], err, 0)) return cudaErrorInvalidValue;
+    if (r.tma_store) {  // D: box {32 columns, 32 rows}, 64B swizzle (one epilogue warp's chunk)
+      const DeviceMat dm{r.D, (int64_t)r.M, (int64_t)r.N, r.ldd};
+      if (!ctx.tmap(dm, 32, &tm.m[q][4], err, 64)) return cudaErrorInvalidValue;
     }
     Prob& p = g.p[q];
     p.M = r.M;
@@ -297,20 +329,27 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
     p.fix_bf16 = r.fix_bf16;
     p.fix_transpose = r.fix_transpose;
     p.fix_accumulate = r.fix_accumulate;
-    p.dep_flags = r.dep_flags;
-    p.pub_flags = r.pub_flags;
-    p.epoch = r.epoch;
-    p.hint_a = r.a_stream_once ? kEvictFirst : kEvictNormal;
+    p.fold = r.fold;
+    p.fold_w = r.fold_w;
+    if (r.out_mode == OUT_F32_FOLD &&
+        (!(r.fold_w == 8 || r.fold_w == 16 || r.fold_w == 32) || r.fold * r.fold_w != r.BN || r.BN > 256)) {
+      if (err) *err = "tc_gemm: OUT_F32_FOLD needs fold_w in {8, 16, 32} and BN = fold * fold_w";
+      return cudaErrorInvalidValue;
+    }
+    p.tail_diag = r.tail_diag ? 1 : 0;
+    p.hint_a = r.a_policy == 1 ? kEvictNormal : r.a_policy == 2 ? kEvictFirst
+               : r.a_stream_once ? kEvictFirst : kEvictNormal;
     p.hint_b = kEvictLast;
     g.total_units += p.units;
     if (r.BN > bn_max) bn_max = r.BN;
   }
   g.nprob = nreq;
+  g.trace = (ctx.trace && ctx.trace_kid == reqs[0].kid && g.total_units <= Ctx::kTraceUnits) ? ctx.trace : nullptr;
   if (const char* d = getenv("RUNLORA_DBG_GEMM")) g.dbg = atoi(d);
   for (int q = nreq; q < kMaxProb; ++q) g.p[q] = g.p[0], g.p[q].units = 0;
   if (g.total_units <= 0) return cudaSuccess;
   ctx.launch_begin(s, reqs[0].kid);
-  cudaError_t e = dispatch_tc(ctx, bn_max, cg, ctx.occ2() && reqs[0].a_stream_once, tm, g, s);
+  cudaError_t e = dispatch_tc(ctx, bn_max, cg, ctx.occ2() && reqs[0].a_stream_once, tma_store, tm, g, s);
   ctx.launch_end(s);
   if (e != cudaSuccess && err) *err = std::string("tc_gemm launch: ") + cudaGetErrorString(e);
   return e;
@@ -332,6 +371,19 @@ cudaError_t launch_splitk_reduce(Ctx& ctx, const ReduceJob* jobs, int njobs, cud
   if (blocks > cap) blocks = cap;
   ctx.launch_begin(s, KID_SPLITK_REDUCE);
   cudaError_t e = launch_pdl(ctx, splitk_reduce_kernel, dim3((unsigned)blocks), dim3(256), s, a);
+  ctx.launch_end(s);
+  return e;
+}
+
+cudaError_t launch_repeat_cols(Ctx& ctx, const void* src, int rows, int cols, int reps, void* dst, cudaStream_t s) {
+  if (cols % 8 != 0) return cudaErrorInvalidValue;  // 16-byte groups of bf16
+  const int g = cols / 8;
+  const long long total = (long long)rows * g * reps;
+  long long blocks = (total + 255) / 256;
+  if (blocks > ctx.num_sms() * 8LL) blocks = ctx.num_sms() * 8LL;
+  ctx.launch_begin(s, KID_REPEAT_COLS);
+  cudaError_t e = launch_pdl(ctx, repeat_cols_kernel, dim3((unsigned)blocks), dim3(256), s,
+                             static_cast<const uint4*>(src), rows, g, reps, static_cast<uint4*>(dst));
   ctx.launch_end(s);
   return e;
 }

@@ -304,6 +304,79 @@ Skinny job_dB_dense(const runlora_shape_t& s, const void* z2d, const void* A, vo
   return Skinny{mat(z2d, s.k, s.m), true, mat(A, s.k, s.r), true, s.m, s.k, s.r, dB, gb, s.m, true, acc};
 }
 
+// Backward1/5 adapter gradients (Alg. 1 lines 1-4 / Alg. 5 lines 1-4)
+// in two launches that keep every CTA slot streaming:
+//   projections   Z1 = dY·Bᵀ, Z2 = X·A, split over K (m for Z1, k for Z2) into sz bf16
+//                 partials stored side by side, Zp = [Z_0 | .. | Z_{sz-1}] (n x sz*r), so no
+//                 split-K fix-up sits on the epilogue path;
+//   reductions    dA = Xᵀ·Z1 = Σ_s Xᵀ·Z1_s and dBᵀ = dYᵀ·Z2: ONE MMA against all blocks
+//                 (N = sz*r), the epilogue folds the sz column blocks in fixed order; split
+//                 over tokens into fp32 slabs summed by the deterministic reducer.
+// backward1's dX tail then reads Zp against A repeated sz times (Σ_s Z1_s·Aᵀ).
+// The plan is a pure function of the shape (and environment), so backward_input knows
+// which Z1 layout backward_params left in the workspace.
+struct ZPlan {
+  bool ok;
+  int sz, kpz[2];        // projection K-splits (Z1, Z2 alike) and k-blocks per split
+  int bn_z[2];           // MMA N of the projections
+  int bn_t;              // MMA N of the reductions (sz * r when the partials are folded)
+  int tsplits, kpt;      // token-reduction splits and k-blocks (64 tokens) per split
+  size_t off[2], bytes;  // fp32 slab regions: dA, dB
+};
+
+ZPlan plan_z(const runlora_shape_t& s) {
+  ZPlan f{};
+  if (s.dtype != RUNLORA_BF16) return f;
+  const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
+  const int64_t mt = (n + kBM - 1) / kBM;
+  const int64_t nkb_n = (n + kBK - 1) / kBK;
+  f.bn_z[0] = skinny_bn(r, false);  // Z1: B_op = Bᵀ from B [r, m] (K-major)
+  f.bn_z[1] = skinny_bn(r, true);   // Z2: B_op = A [k, r] (MN-major)
+  if (r > f.bn_z[0] || r > f.bn_z[1]) return f;  // one n tile per projection
+  // sz: split K only while the projections' 2*mt row tiles leave SMs idle (2*mt*sz <= one
+  // wave of 2 CTAs/SM), within sz*r in {16, 32, 64} (a legal MN-major tile width that keeps
+  // the reductions on the 2-CTA/SM kernel) and r a fold width (8, 16, 32).  Measured at C2
+  // (mt = 64): sz = 1 and sz = 2 give the same step time, so the plain layout is kept there.
+  const int64_t kbz[2] = {(m + kBK - 1) / kBK, (k + kBK - 1) / kBK};
+  int sz = 1;
+  if ((r == 8 || r == 16 || r == 32) && 2 * mt < 148) {
+    for (int c = 2; c <= 8 && 2 * mt * c <= 2 * 148; c *= 2) {
+      if (c * r > 64) break;
+      bool even = true;
+      for (int i = 0; i < 2; ++i) {
+        const int64_t kp = (kbz[i] + c - 1) / c;
+        even = even && (kbz[i] + kp - 1) / kp == c;
+      }
+      if (!even) break;
+      sz = c;
+    }
+  }
+  if (const char* e = getenv("RUNLORA_ZSPLIT")) sz = std::max(1, atoi(e));
+  f.sz = sz;
+  for (int i = 0; i < 2; ++i) {
+    f.kpz[i] = (int)((kbz[i] + sz - 1) / sz);
+    if ((kbz[i] + f.kpz[i] - 1) / f.kpz[i] != sz) return f;
+  }
+  f.bn_t = sz > 1 ? (int)(sz * r) : skinny_bn(r, true);
+  if (r > f.bn_t || f.bn_t > 256) return f;
+  // token splits: as many as fit in one wave of CTA slots
+  const int64_t tiles = (k + kBM - 1) / kBM + (m + kBM - 1) / kBM;
+  int64_t ts = std::max<int64_t>(1, (2 * 148) / tiles);
+  ts = std::min<int64_t>({ts, 32, nkb_n});
+  f.kpt = (int)((nkb_n + ts - 1) / ts);
+  f.tsplits = (int)((nkb_n + f.kpt - 1) / f.kpt);
+  const size_t w = sz > 1 ? (size_t)r : (size_t)f.bn_t;  // slab row width (folded: r)
+  size_t off = 0;
+  f.off[0] = off;
+  off += al((size_t)f.tsplits * (size_t)k * w * 4);
+  f.off[1] = off;
+  off += al((size_t)f.tsplits * (size_t)m * w * 4);
+  f.bytes = off;
+  f.ok = true;
+  (void)mt;
+  return f;
+}
+
 size_t partial_need(const runlora_shape_t& s) {
   // every skinny launch group any variant issues; the P region covers the largest
   const void* d = reinterpret_cast<const void*>(256);
@@ -319,28 +392,35 @@ size_t partial_need(const runlora_shape_t& s) {
   const int counts[8] = {1, 2, 2, 1, 2, 2, 0, 0};
   size_t need = 0;
   for (int i = 0; i < 6; ++i) need = std::max(need, plan_skinny(g[i], counts[i]).p_bytes);
+  const ZPlan f = plan_z(s);
+  if (f.ok) need = std::max(need, f.bytes);
   return need;
 }
 
 // ------------------------------------------------------------ workspace layout
 struct Layout {
-  size_t z1, z2, wp, p, total;
+  size_t z1, z2, arep, wp, p, total;
 };
 
+// Z1, Z2: n x r (or n x sz*r partial blocks, see ZPlan); arep: A repeated sz times along its
+// columns (k x sz*r, the dX concat tail against Z1's partial blocks).
 Layout layout_of(const runlora_shape_t& s) {
   const size_t es = s.dtype == RUNLORA_BF16 ? 2 : 4;
   const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
+  const ZPlan f = plan_z(s);
+  const size_t zc = (size_t)r * (f.ok ? f.sz : 1);
   Layout L;
   L.z1 = 0;
-  L.z2 = al((size_t)n * r * es);
-  L.wp = L.z2 + al((size_t)n * r * es);
+  L.z2 = al((size_t)n * zc * es);
+  L.arep = L.z2 + al((size_t)n * zc * es);
+  L.wp = L.arep + (f.ok && f.sz > 1 ? al((size_t)k * zc * es) : 0);
   L.p = L.wp + al((size_t)k * m * es);
   L.total = L.p + (s.dtype == RUNLORA_BF16 ? partial_need(s) : 0);
   return L;
 }
 
 struct Bufs {
-  void *z1, *z2, *wp;
+  void *z1, *z2, *arep, *wp;
   float* P;
 };
 
@@ -356,6 +436,7 @@ runlora_status_t bind_ws(const runlora_shape_t& s, void* ws, size_t ws_bytes, Bu
   char* base = static_cast<char*>(ws);
   b->z1 = base + L.z1;
   b->z2 = base + L.z2;
+  b->arep = base + L.arep;
   b->wp = base + L.wp;
   b->P = reinterpret_cast<float*>(base + L.p);
   return RUNLORA_OK;
@@ -368,28 +449,35 @@ runlora_status_t gemm(Ctx& c, const GemmReq& q, cudaStream_t st) {
   return RUNLORA_OK;
 }
 
-// W' = W + A·B  (k×m, bf16, formed in fp32 in TMEM and rounded once).
+// W' = W + A·B  (k×m, bf16, formed in fp32 in TMEM and rounded once; Eq. 2).
+// ONE GEMM D = [A | I]·[B ; W_rows(tile)]: the K = r product plus a block-diagonal identity
+// tail that brings W's rows of the output tile into the same fp32 accumulator through the
+// tensor cores (1.0·w is exact), so the epilogue is a plain (TMA) store.
 runlora_status_t wprime_bf16(Ctx& c, const runlora_shape_t& s, const void* W, const void* A, const void* B, void* Wp,
                              cudaStream_t st) {
   GemmReq q = base_req((int)s.k, (int)s.m, KID_GEMM_WPRIME);
   q.a = mat(A, s.k, s.r);  // A_op[M=k, K=r], K-major
-  q.a_mn = false;
   q.b = mat(B, s.r, s.m);  // B_op[K=r, N=m] stored [K, N]: MN-major
   q.b_mn = true;
   q.K1 = (int)s.r;
-  q.out_mode = OUT_BF16_ADD;
-  q.Cin = W;
-  q.ldc = s.m;
+  q.a2 = mat(c.identity(), 128, 128);
+  q.b2 = mat(W, s.k, s.m);  // B2_op[K=i, N=j] = W[i, j]: MN-major, rows of the tile
+  q.K2 = 128;
+  q.tail_diag = true;
+  q.out_mode = OUT_BF16;
   q.D = Wp;
   q.ldd = s.m;
   q.BN = 256;
+  q.tma_store = c.tma_store_wprime();
   return gemm(c, q, st);
 }
 
 // W'ᵀ = (W + A·B)ᵀ  (m×k, bf16) for forward2: stored K-major for the Y GEMM's B operand
 // (the tensor cores stream K-major B faster than MN-major B).  GEMM M = m,
-// N = k, K = r: A_op = Bᵀ (B stored [r, m]: MN-major), B_op = Aᵀ (A stored [k, r]:
-// K-major); the epilogue adds W transposed through shared memory.
+// N = k: D[j, i] = Σ_r B[r, j]·A[i, r] + Σ_j' I[j, j']·W[i, j'] — A_op = Bᵀ (B stored [r, m]:
+// MN-major), B_op = Aᵀ (A stored [k, r]: K-major); the tail B operand W[i][j'] is K-major
+// (K = j' contiguous), read at this tile's rows j' = m0.. (I is symmetric, so it serves as
+// the MN-major A operand too).
 runlora_status_t wprime_t_bf16(Ctx& c, const runlora_shape_t& s, const void* W, const void* A, const void* B,
                                void* Wpt, cudaStream_t st) {
   GemmReq q = base_req((int)s.m, (int)s.k, KID_GEMM_WPRIME);
@@ -398,12 +486,15 @@ runlora_status_t wprime_t_bf16(Ctx& c, const runlora_shape_t& s, const void* W, 
   q.b = mat(A, s.k, s.r);
   q.b_mn = false;
   q.K1 = (int)s.r;
-  q.out_mode = OUT_BF16_ADD_T;
-  q.Cin = W;
-  q.ldc = s.m;
+  q.a2 = mat(c.identity(), 128, 128);
+  q.b2 = mat(W, s.k, s.m);
+  q.K2 = 128;
+  q.tail_diag = true;
+  q.out_mode = OUT_BF16;
   q.D = Wpt;
   q.ldd = s.k;
   q.BN = 256;
+  q.tma_store = c.tma_store_wprime();
   return gemm(c, q, st);
 }
 
@@ -413,6 +504,7 @@ GemmReq main_req(Ctx& c, int M, int N) {
   q.BN = 256;
   q.cg = c.main_cg();
   q.out_mode = OUT_BF16;
+  q.tma_store = c.tma_store_main() && q.cg == 2;
   return q;
 }
 
@@ -435,80 +527,87 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
     q.a2 = mat(b.z2, n, r);
     q.b2 = mat(B, r, m);
     q.K2 = (int)r;
-  } else if (c.wprime_t()) {
+  } else {
     RL_TRY(wprime_t_bf16(c, s, W, A, B, b.wp, st));  // W'ᵀ [m, k]
     q.b = mat(b.wp, m, k);
     q.b_mn = false;
-  } else {
-    RL_TRY(wprime_bf16(c, s, W, A, B, b.wp, st));
-    q.b = mat(b.wp, k, m);
   }
   return gemm(c, q, st);
 }
 
-// backward1/5 adapter gradients in ONE launch: the Z1 = dY·Bᵀ and Z2 = X·A tiles are
-// scheduled first and publish a per-128-token flag; the dA = Xᵀ·Z1 / dBᵀ = dYᵀ·Z2 split-K
-// units of the same persistent launch wait only for the Z rows of their own token range.
-// Returns false (nothing launched) when the projections would not write bf16 directly.
-bool fused_grads_bf16(Ctx& c, const runlora_shape_t& s, const void* X, const void* A, const void* B, const void* dY,
-                      void* dA, void* dB, bool gb, bool acc, Bufs& b, cudaStream_t st, bool defer,
-                      runlora_status_t* status) {
-  Skinny pj[2] = {job_Z1(s, dY, B, b.z1), job_Z2(s, X, A, b.z2)};
-  Skinny tj[2] = {job_dA_tok(s, X, b.z1, dA, gb, acc), job_dB_tok(s, dY, b.z2, dB, gb, acc)};
-  const SkinnyPlan pp = plan_skinny(pj, 2);
-  const SkinnyPlan tp = plan_skinny(tj, 2);
-  const int64_t mt = (s.n + kBM - 1) / kBM;
-  if (!c.fused_grads() || !c.flags() || !pp.direct || tp.direct || 2 * mt > Ctx::kCounterCap / 2) return false;
-  const unsigned epoch = c.next_epoch();
-  int* f1 = c.flags();
-  int* f2 = f1 + mt;
-  GemmReq q[4];
-  ReduceJob rj[2];
-  for (int i = 0; i < 2; ++i) {
-    const Skinny& j = pj[i];
-    q[i] = base_req((int)j.rows, (int)j.r, KID_GEMM_GRADS);
-    q[i].a = j.a;
-    q[i].a_mn = j.a_mn;
-    q[i].b = j.b;
-    q[i].b_mn = j.b_mn;
-    q[i].K1 = (int)j.K;
-    q[i].BN = pp.BN[i];
-    q[i].a_stream_once = true;
-    q[i].out_mode = OUT_BF16;
-    q[i].D = j.out;
-    q[i].ldd = j.ldo;
-    q[i].pub_flags = i == 0 ? f1 : f2;
-    q[i].epoch = epoch;
-  }
-  for (int i = 0; i < 2; ++i) {
-    const Skinny& j = tj[i];
-    GemmReq& r = q[2 + i];
-    r = base_req((int)j.rows, tp.Npad[i], KID_GEMM_TOKRED);
-    r.a = j.a;
-    r.a_mn = j.a_mn;
-    r.b = j.b;
-    r.b_mn = j.b_mn;
-    r.K1 = (int)j.K;
-    r.BN = tp.BN[i];
-    r.a_stream_once = true;
-    float* Pi = reinterpret_cast<float*>(reinterpret_cast<char*>(b.P) + tp.p_off[i]);
-    r.out_mode = OUT_F32;
-    r.D = Pi;
-    r.ldd = tp.Npad[i];
-    r.split_stride = j.rows * (int64_t)tp.Npad[i];
-    r.splits = tp.splits[i];
-    r.kb_per_split = tp.kps[i];
-    r.dep_flags = i == 0 ? f1 : f2;
-    r.epoch = epoch;
-    rj[i] = ReduceJob{Pi, tp.splits[i], r.split_stride, (int)j.rows, (int)j.r, tp.Npad[i], j.out, j.out_bf16 ? 1 : 0,
-                      j.ldo, j.transpose ? 1 : 0, j.accumulate ? 1 : 0};
-  }
+// backward1/5 adapter gradients: projections launch, reductions launch, reducer (see ZPlan).
+runlora_status_t grads_tok_bf16(Ctx& c, int v, const ZPlan& f, const runlora_shape_t& s, const void* X,
+                                const void* A, const void* B, const void* dY, void* dA, void* dB, bool gb, bool acc,
+                                Bufs& b, cudaStream_t st, bool defer) {
+  const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
+  const int zc = (int)(r * f.sz);  // columns of the partial-Z matrices
   std::string err;
-  cudaError_t e = launch_tc_gemm(c, q, 4, st, &err);
-  if (e != cudaSuccess) {
-    *status = fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
-    return true;
+  if (v == 1 && f.sz > 1) {
+    // A repeated sz times for backward1's dX tail, on the side stream under the projections
+    cudaStream_t ss = c.side_stream();
+    cudaEventRecord(c.fork_event(), st);
+    cudaStreamWaitEvent(ss, c.fork_event(), 0);
+    cudaError_t e = launch_repeat_cols(c, A, (int)k, (int)r, f.sz, b.arep, ss);
+    if (e != cudaSuccess) return cuda_fail(e, "repeat_cols launch");
+    cudaEventRecord(c.arep_event(), ss);
   }
+  // projections: Zp[:, s*r:(s+1)*r] = K-split s of dY·Bᵀ / X·A (bf16)
+  GemmReq q[2];
+  const DeviceMat za[2] = {mat(dY, n, m), mat(X, n, k)};
+  const DeviceMat zb[2] = {mat(B, r, m), mat(A, k, r)};
+  void* zout[2] = {b.z1, b.z2};
+  for (int i = 0; i < 2; ++i) {
+    GemmReq& g = q[i];
+    g = base_req((int)n, (int)r, KID_GEMM_PROJ);
+    g.a = za[i];
+    g.b = zb[i];
+    g.b_mn = i == 1;
+    g.K1 = (int)(i == 0 ? m : k);
+    g.BN = f.bn_z[i];
+    g.a_stream_once = true;
+    g.out_mode = OUT_BF16;
+    g.D = zout[i];
+    g.ldd = zc;
+    g.split_stride = r;  // split s -> column block s
+    g.splits = f.sz;
+    g.kb_per_split = f.kpz[i];
+  }
+  cudaError_t e = launch_tc_gemm(c, q, 2, st, &err);
+  if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
+  // reductions: dA = Σ_s Xᵀ·Z1_s, dBᵀ = Σ_s dYᵀ·Z2_s (token splits -> fp32 slabs)
+  ReduceJob rj[2];
+  const DeviceMat ta[2] = {mat(X, n, k), mat(dY, n, m)};
+  const int64_t rows[2] = {k, m};
+  void* outs[2] = {dA, dB};
+  for (int i = 0; i < 2; ++i) {
+    GemmReq& g = q[i];
+    g = base_req((int)rows[i], f.sz > 1 ? f.bn_t : (int)r, KID_GEMM_TOKRED);
+    g.a = ta[i];
+    g.a_mn = true;
+    g.b = mat(zout[i], n, zc);
+    g.b_mn = true;
+    g.K1 = (int)n;
+    g.BN = f.bn_t;
+    g.a_stream_once = true;
+    float* P = reinterpret_cast<float*>(reinterpret_cast<char*>(b.P) + f.off[i]);
+    g.D = P;
+    g.splits = f.tsplits;
+    g.kb_per_split = f.kpt;
+    if (f.sz > 1) {
+      g.out_mode = OUT_F32_FOLD;
+      g.fold = f.sz;
+      g.fold_w = (int)r;
+      g.ldd = r;
+    } else {
+      g.out_mode = OUT_F32;
+      g.ldd = f.bn_t;  // plain slabs keep the padded tile width
+    }
+    g.split_stride = rows[i] * g.ldd;
+    rj[i] = ReduceJob{P, f.tsplits, g.split_stride, (int)rows[i], (int)r, g.ldd, outs[i], gb ? 1 : 0,
+                      i == 0 ? r : m, i == 1 ? 1 : 0, acc ? 1 : 0};
+  }
+  e = launch_tc_gemm(c, q, 2, st, &err);
+  if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
   cudaStream_t rs = st;
   if (defer) {
     rs = c.side_stream();
@@ -516,16 +615,12 @@ bool fused_grads_bf16(Ctx& c, const runlora_shape_t& s, const void* X, const voi
     cudaStreamWaitEvent(rs, c.fork_event(), 0);
   }
   e = launch_splitk_reduce(c, rj, 2, rs);
-  if (e != cudaSuccess) {
-    *status = cuda_fail(e, "splitk_reduce launch");
-    return true;
-  }
+  if (e != cudaSuccess) return cuda_fail(e, "splitk_reduce launch");
   if (defer) {
     cudaEventRecord(c.join_event(), rs);
     c.join_pending = true;
   }
-  *status = RUNLORA_OK;
-  return true;
+  return RUNLORA_OK;
 }
 
 runlora_status_t params_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* X, const void* A, const void* B,
@@ -533,8 +628,8 @@ runlora_status_t params_bf16(Ctx& c, int v, const runlora_shape_t& s, const void
                              bool defer = false) {
   const int64_t n = s.n, k = s.k, m = s.m;
   if (v == 1 || v == 5) {  // Alg. 1 / Alg. 5: Z1, Z2 | dA = Xᵀ·Z1, dB = Z2ᵀ·dY
-    runlora_status_t fst;
-    if (fused_grads_bf16(c, s, X, A, B, dY, dA, dB, gb, acc, b, st, defer, &fst)) return fst;
+    const ZPlan f = plan_z(s);
+    if (f.ok) return grads_tok_bf16(c, v, f, s, X, A, B, dY, dA, dB, gb, acc, b, st, defer);
     Skinny pj[2] = {job_Z1(s, dY, B, b.z1), job_Z2(s, X, A, b.z2)};
     RL_TRY(run_skinny(c, pj, 2, b.P, KID_GEMM_PROJ, st));
     Skinny tj[2] = {job_dA_tok(s, X, b.z1, dA, gb, acc), job_dB_tok(s, dY, b.z2, dB, gb, acc)};
@@ -582,6 +677,16 @@ runlora_status_t input_bf16(Ctx& c, int v, const runlora_shape_t& s, const void*
     q.a2 = mat(b.z1, n, r);
     q.b2 = mat(A, k, r);  // Aᵀ stored [N=k, K=r] = A: K-major
     q.K2 = (int)r;
+    const ZPlan f = plan_z(s);
+    if (v == 1 && f.ok && f.sz > 1) {
+      // backward1's adapter-gradient pass left Z1 as sz partial blocks: dY·Wᵀ + Σ_s Z1_s·Aᵀ =
+      // [dY | Z1_0 | .. | Z1_{sz-1}]·[Wᵀ ; Aᵀ ; .. ; Aᵀ]
+      const int zc = (int)(r * f.sz);
+      cudaStreamWaitEvent(st, c.arep_event(), 0);  // A_rep, built by backward_params
+      q.a2 = mat(b.z1, n, zc);
+      q.b2 = mat(b.arep, k, zc);
+      q.K2 = zc;
+    }
   } else {  // dX = dY·W'ᵀ
     RL_TRY(wprime_bf16(c, s, W, A, B, b.wp, st));
     q.b = mat(b.wp, k, m);
@@ -784,6 +889,11 @@ runlora_status_t runlora_create(runlora_handle_t* out, int device) {
   try {
     runlora_handle_s* h = new runlora_handle_s;
     h->ctx = new Ctx(device);
+    if (!h->ctx->identity() || !h->ctx->counters()) {
+      delete h->ctx;
+      delete h;
+      return fail(RUNLORA_ERR_CUDA, "device allocation of the handle's identity tile / counters failed");
+    }
     *out = h;
   } catch (...) {
     return fail(RUNLORA_ERR_INVALID_ARG, "allocation of handle failed");
@@ -1057,4 +1167,15 @@ extern "C" runlora_status_t runlora_debug_gemm(runlora_handle_t h, int M, int N,
   DeviceGuard dg(h->ctx->device());
   RL_TRY(gemm(*h->ctx, q, static_cast<cudaStream_t>(stream)));
   return post_launch();
+}
+
+// Copies the debug timeline of the last traced launch (env RUNLORA_TRACE=<kernel id>) to
+// host memory: 8 uint64 per unit (see GemmArgs::trace).  Returns the number of units copied.
+extern "C" int runlora_debug_trace(runlora_handle_t h, unsigned long long* host, int max_units) {
+  if (!h || !h->ctx || !h->ctx->trace || !host) return 0;
+  const int n = std::min(max_units, Ctx::kTraceUnits);
+  DeviceGuard dg(h->ctx->device());
+  if (cudaMemcpy(host, h->ctx->trace, sizeof(unsigned long long) * 8 * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 0;
+  return n;
 }

@@ -35,9 +35,12 @@
 
 namespace runlora {
 
-enum OutMode : int { OUT_BF16 = 0, OUT_BF16_ADD = 1, OUT_F32 = 2, OUT_BF16_ADD_T = 3 };
+enum OutMode : int { OUT_BF16 = 0, OUT_BF16_ADD = 1, OUT_F32 = 2, OUT_F32_FOLD = 4 };
+// OUT_BF16 with splits: split s of the K reduction writes its own bf16 partial at
+//                 D + s * split_stride (e.g. side-by-side column blocks of a partial matrix).
+// OUT_F32_FOLD:   the accumulator's bn = fold * fold_w columns are fold column blocks whose sum
+//                 (fixed block order, fp32) is the output: fp32 slab D[split][M][ldd], fold_w cols.
 // OUT_BF16_ADD:   D[i, j] = acc[i, j] + Cin[i * ldc + j]
-// OUT_BF16_ADD_T: D[i, j] = acc[i, j] + Cin[j * ldc + i]   (transposed add; EPI = 2 kernels)
 
 struct Prob {
   int M, N;              // output extent (epilogue masks rows >= M, cols >= N)
@@ -69,13 +72,12 @@ struct Prob {
   void* fix_out;
   long long fix_ldo;
   int fix_bf16, fix_transpose, fix_accumulate;
-  // Dataflow between problems of one launch (fused adapter-gradient pass): a unit of this
-  // problem covering K rows [kb0*64, kb1*64) first waits until dep_flags[t] == epoch for
-  // every 128-row tile t of the problem that produces its B operand; a problem with
-  // pub_flags publishes pub_flags[m_blk] = epoch once its tile's rows are stored.
-  int* dep_flags;
-  int* pub_flags;
-  unsigned epoch;
+  int fold, fold_w;  // OUT_F32_FOLD
+  // Block-diagonal concat-K tail: the tail A operand is the 128x128 identity (A2, loaded at
+  // M coordinate 0) and the tail B operand is read at K coordinate m0 + k, i.e. the rows of
+  // B2 that belong to this tile's own M range.  D += I·B2[m0.., n0..] adds a matrix that is
+  // indexed like the output (W + A·B: the add rides in the mainloop, exact in fp32).
+  int tail_diag;
 };
 
 constexpr int kMaxProb = 4;
@@ -85,10 +87,13 @@ struct GemmArgs {
   int nprob;
   int total_units;
   int dbg;  // 0 normal; 1: no TMA (MMA-only); 2: no MMA (TMA-only); 3: as 1 + no stores; 4: as 1 + no epilogue
+  // Debug timeline (RUNLORA_TRACE): per unit u, trace[8u + {0: producer start, 2: last load
+  // issued, 3: epilogue done, 4: CTA, 5: problem}] (%globaltimer ns).
+  unsigned long long* trace;
 };
 
-struct Tmaps {  // per problem: A1, B1, A2, B2
-  CUtensorMap m[kMaxProb][4];
+struct Tmaps {  // per problem: A1, B1, A2, B2, D (EPI = 3: TMA-store epilogue)
+  CUtensorMap m[kMaxProb][5];
 };
 
 constexpr int kBM = 128;  // rows per CTA
@@ -96,19 +101,20 @@ constexpr int kBK = 64;
 constexpr int kGemmThreads = 256;
 
 // OCC = CTAs per SM (2 for the HBM-bound rank-r kernels: twice the TMA requests in flight).
-// EPI = 2 (transposed add): the epilogue stages the BN x 128 block of Cin in smem.
+// EPI = 3: TMA-store epilogue (bf16 tile staged per warp in swizzled smem).
 template <int BN_MAX, int CG, int OCC = 1, int EPI = 0>
 struct TileCfg {
   static constexpr uint32_t A_BYTES = kBM * kBK * 2;
   static constexpr uint32_t B_BYTES = (BN_MAX / CG) * kBK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr uint32_t CT_BYTES = EPI == 2 ? 2 * BN_MAX * kBM * 2 : 0;  // double-buffered Cin block
+  // EPI = 3: per epilogue warp two 32-row x 32-column bf16 staging tiles (64B swizzle) for TMA stores
+  static constexpr uint32_t STG_BYTES = EPI == 3 ? 4 * 2 * 2048 : 0;
   // up to ~225 KB of the 227 KB opt-in smem per SM (7 stages for the 256x256 pair tiles)
-  static constexpr int STAGES_RAW = ((OCC == 1 ? 225 : 110) * 1024 - CT_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES_RAW = ((OCC == 1 ? 225 : 110) * 1024 - STG_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = (2 * BN_MAX <= 32) ? 32 : (2 * BN_MAX <= 64) ? 64
                                         : (2 * BN_MAX <= 128) ? 128 : (2 * BN_MAX <= 256) ? 256 : 512;
-  static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + CT_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + STG_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 struct Unit {
@@ -168,7 +174,7 @@ __device__ __forceinline__ void store_row_segment(const Prob& p, int split, int 
       }
     }
   } else {
-    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.D) + (long long)row * p.ldd + col;
+    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.D) + split * p.split_stride + (long long)row * p.ldd + col;
     const bool add = p.out_mode == OUT_BF16_ADD;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -202,7 +208,7 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: 
 
 // Deterministic split-K fix-up, run by the 128 epilogue threads after their unit's fp32
 // slab is stored: the last-arriving unit of the tile reduces all slabs in split order.
-__device__ __forceinline__ void splitk_fixup(const Prob& p, const Unit& t, int m0, int n0, int row, int* s_flag) {
+__device__ __forceinline__ bool splitk_fixup(const Prob& p, const Unit& t, int m0, int n0, int row, int* s_flag) {
   __threadfence();
   epi_bar();
   const int tile = t.m_blk * p.num_n_tiles + t.n_blk;
@@ -213,48 +219,66 @@ __device__ __forceinline__ void splitk_fixup(const Prob& p, const Unit& t, int m
   epi_bar();
   const int last = *s_flag;
   epi_bar();  // everyone has read the flag before it can be rewritten for the next unit
-  if (!last) return;
+  if (!last) return false;
   __threadfence();
   if (row < p.M) {
+    // up to 4 splits x 4 column groups (16 loads) in flight, summed in split order
     const int c_end = min(n0 + p.bn, p.fix_cols);
-    for (int c = n0; c < c_end; c += 4) {
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      const float* src = static_cast<const float*>(p.D) + (long long)row * p.ldd + c;
-      for (int sp = 0; sp < p.num_splits; ++sp) {
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(src + sp * p.split_stride));
-        acc.x += v.x;
-        acc.y += v.y;
-        acc.z += v.z;
-        acc.w += v.w;
-      }
-      const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+    const float* src = static_cast<const float*>(p.D) + (long long)row * p.ldd;
+    for (int c = n0; c < c_end; c += 16) {
+      float4 acc[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        if (c + e >= c_end) break;
-        const long long o = p.fix_transpose ? (long long)(c + e) * p.fix_ldo + row : (long long)row * p.fix_ldo + c + e;
-        float v = a4[e];
-        if (p.fix_bf16) {
-          __nv_bfloat16* d = static_cast<__nv_bfloat16*>(p.fix_out) + o;
-          if (p.fix_accumulate) v += __bfloat162float(*d);
-          *d = __float2bfloat16_rn(v);
-        } else {
-          float* d = static_cast<float*>(p.fix_out) + o;
-          if (p.fix_accumulate) v += *d;
-          *d = v;
+      for (int gi = 0; gi < 4; ++gi) acc[gi] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s0 = 0; s0 < p.num_splits; s0 += 4) {
+        float4 v[4][4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int gi = 0; gi < 4; ++gi)
+            if (s0 + x < p.num_splits && c + 4 * gi < c_end)
+              v[x][gi] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + x) * p.split_stride + c + 4 * gi));
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int gi = 0; gi < 4; ++gi)
+            if (s0 + x < p.num_splits && c + 4 * gi < c_end) {
+              acc[gi].x += v[x][gi].x;
+              acc[gi].y += v[x][gi].y;
+              acc[gi].z += v[x][gi].z;
+              acc[gi].w += v[x][gi].w;
+            }
+      }
+#pragma unroll
+      for (int gi = 0; gi < 4; ++gi) {
+        const float a4[4] = {acc[gi].x, acc[gi].y, acc[gi].z, acc[gi].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int col = c + 4 * gi + e;
+          if (col >= c_end) break;
+          const long long o = p.fix_transpose ? (long long)col * p.fix_ldo + row : (long long)row * p.fix_ldo + col;
+          float v = a4[e];
+          if (p.fix_bf16) {
+            __nv_bfloat16* d = static_cast<__nv_bfloat16*>(p.fix_out) + o;
+            if (p.fix_accumulate) v += __bfloat162float(*d);
+            *d = __float2bfloat16_rn(v);
+          } else {
+            float* d = static_cast<float*>(p.fix_out) + o;
+            if (p.fix_accumulate) v += *d;
+            *d = v;
+          }
         }
       }
     }
   }
   if (threadIdx.x == 4 * 32) p.counters[tile] = 0;  // ready for the next launch
+  return true;
 }
 
-// EPI = 1: W + A·B (prefetches the 256-column W segment of each row);
-// EPI = 2: (W + A·B)ᵀ written directly (transposed add through a smem block of W).
+// EPI = 0: epilogue stores from registers; EPI = 3: TMA-store epilogue (plain bf16 outputs).
 template <int BN_MAX, int CG, int OCC = 1, int EPI = 0>
 __global__ void __launch_bounds__(kGemmThreads, OCC)
     tc_gemm_kernel(const __grid_constant__ Tmaps tm, const __grid_constant__ GemmArgs g) {
   using C = TileCfg<BN_MAX, CG, OCC, EPI>;
-  constexpr bool WADD = EPI == 1;
   constexpr int STAGES = C::STAGES;
   static_assert(BN_MAX % (16 * CG) == 0 && BN_MAX >= 16 && BN_MAX <= 256, "UMMA N");
 
@@ -267,12 +291,6 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  // EPI = 2: two Cin blocks [BN_MAX rows (output cols)][128 (output rows)] bf16 (TMA-filled
-  // by the producer, one per tile, double-buffered), then their full/empty barriers.
-  __nv_bfloat16* sCt = reinterpret_cast<__nv_bfloat16*>(smem + STAGES * C::STAGE_BYTES + 256);
-  uint64_t* ct_full = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // 2 barriers, then 2 more
-  uint64_t* ct_empty = ct_full + 2;
-
   __shared__ int s_flag[1];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -285,6 +303,8 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
     for (int q = 0; q < g.nprob; ++q)
       for (int j = 0; j < 4; ++j)
         if (j < 2 || g.p[q].nk2 > 0) tma_prefetch_desc(&tm.m[q][j]);
+    if constexpr (EPI == 3)
+      for (int q = 0; q < g.nprob; ++q) tma_prefetch_desc(&tm.m[q][4]);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -292,10 +312,6 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * CG);
-      if constexpr (EPI == 2) {
-        mbar_init(&ct_full[a], 1);
-        mbar_init(&ct_empty[a], 4);
-      }
     }
     fence_mbar_init();
   }
@@ -314,10 +330,16 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
     // The whole warp runs the loop (warp-uniform values); one elected lane issues.
     int stage = 0;
     uint32_t phase = 0;
-    int it_p = 0;  // EPI = 2: Cin block counter
-    for (int u = group; u < g.total_units; u += ngroups) {
+    for (int i_u = 0;; ++i_u) {
+      const int u = group + i_u * ngroups;
+      if (u >= g.total_units) break;
       const Unit t = decode_unit(g, u);
       const Prob& p = g.p[t.prob];
+      if (g.trace && lane == 0) {
+        g.trace[8 * u + 0] = globaltimer();
+        g.trace[8 * u + 4] = blockIdx.x;
+        g.trace[8 * u + 5] = t.prob;
+      }
       const int m0 = t.m_blk * (kBM * CG) + rank * kBM;
       const int nb = p.bn / CG;  // B columns held by this CTA
       const int n0 = t.n_blk * p.bn + rank * nb;
@@ -327,30 +349,8 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       const int nkb = nmain + (t.split == 0 ? p.nk2 : 0);
       // snake: every other round of this CTA walks K backwards, starting where the data it
       // (and its neighbours) just streamed is still in L2
-      const bool rev = p.snake && (((u - group) / ngroups) & 1);
+      const bool rev = p.snake && (i_u & 1);
       if (g.dbg == 1 || g.dbg >= 3) continue;
-      if constexpr (EPI == 2) {
-        const int cb = it_p & 1;
-        mbar_wait(&ct_empty[cb], ((it_p >> 1) & 1) ^ 1);
-        if (elect_one_sync()) {
-          mbar_arrive_expect_tx(&ct_full[cb], BN_MAX * kBM * 2);
-          // Cin rows n0.. (output columns), columns m0.. (output rows); box {128, BN}
-          tma_load_2d(&tm.m[t.prob][2], &ct_full[cb], sCt + cb * BN_MAX * kBM, m0, t.n_blk * p.bn, kEvictFirst);
-        }
-        __syncwarp();
-        ++it_p;
-      }
-      if (p.dep_flags) {
-        // wait for the producer problem's 128-row tiles covering this unit's K rows
-        if (lane == 0) {
-          const int t_lo = (kb0 * kBK) / kBM, t_hi = (kb1 * kBK + kBM - 1) / kBM;
-          for (int tt = t_lo; tt < t_hi; ++tt) {
-            while (ld_acquire_gpu(p.dep_flags + tt) != (int)p.epoch) __nanosleep(64);
-          }
-          fence_proxy_async_global();  // generic-proxy writes -> this thread's TMA reads
-        }
-        __syncwarp();
-      }
       const int cw = p.b_swz >> 1;   // MN-major B chunk width (elements)
       const int cb = p.b_swz * kBK;  // MN-major B chunk bytes (64 K-rows)
       for (int i = 0; i < nkb; ++i) {
@@ -361,24 +361,27 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
           uint64_t* fb = &full[stage];
           if (leader) mbar_arrive_expect_tx(fb, p.stage_tx);
           const bool tail = i >= nmain;
+          const bool diag = tail && p.tail_diag;
           const CUtensorMap* ta = &tm.m[t.prob][tail ? 2 : 0];
           const CUtensorMap* tb = &tm.m[t.prob][tail ? 3 : 1];
           const int ki = rev ? nmain - 1 - i : i;
           const int kc = (tail ? (i - nmain) : (kb0 + ki)) * kBK;
+          const int ma = diag ? 0 : m0;          // identity tail: rows of I
+          const int kcb = diag ? m0 + kc : kc;   // identity tail: B2 rows of this tile
           if (!p.a_mn) {
-            tma_load_2d<CG>(ta, fb, a, kc, m0, p.hint_a);
+            tma_load_2d<CG>(ta, fb, a, kc, ma, p.hint_a);
           } else if (p.a_3d) {
-            tma_load_3d<CG>(ta, fb, a, 0, kc, m0 >> 6, p.hint_a);
+            tma_load_3d<CG>(ta, fb, a, 0, kc, ma >> 6, p.hint_a);
           } else {
-            tma_load_2d<CG>(ta, fb, a, m0, kc, p.hint_a);
-            tma_load_2d<CG>(ta, fb, a + 8192, m0 + 64, kc, p.hint_a);
+            tma_load_2d<CG>(ta, fb, a, ma, kc, p.hint_a);
+            tma_load_2d<CG>(ta, fb, a + 8192, ma + 64, kc, p.hint_a);
           }
           if (!p.b_mn) {
-            tma_load_2d<CG>(tb, fb, b, kc, n0, p.hint_b);
+            tma_load_2d<CG>(tb, fb, b, kcb, n0, p.hint_b);
           } else if (p.b_3d) {
-            tma_load_3d<CG>(tb, fb, b, 0, kc, n0 / cw, p.hint_b);
+            tma_load_3d<CG>(tb, fb, b, 0, kcb, n0 / cw, p.hint_b);
           } else {
-            for (int h = 0; h < nb / cw; ++h) tma_load_2d<CG>(tb, fb, b + h * cb, n0 + cw * h, kc, p.hint_b);
+            for (int h = 0; h < nb / cw; ++h) tma_load_2d<CG>(tb, fb, b + h * cb, n0 + cw * h, kcb, p.hint_b);
           }
         }
         __syncwarp();
@@ -387,6 +390,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
           phase ^= 1;
         }
       }
+      if (g.trace && lane == 0) g.trace[8 * u + 2] = globaltimer();
     }
   } else if (warp == 1 && leader) {
     // ------------------------------------------------------------- MMA issuer
@@ -394,8 +398,9 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
     // lane issues tcgen05.mma / tcgen05.commit.
     int stage = 0;
     uint32_t phase = 0;
-    int it = 0;
-    for (int u = group; u < g.total_units; u += ngroups, ++it) {
+    for (int it = 0;; ++it) {
+      const int u = group + it * ngroups;
+      if (u >= g.total_units) break;
       const Unit t = decode_unit(g, u);
       const Prob& p = g.p[t.prob];
       const int kb0 = t.split * p.kb_per_split;
@@ -404,7 +409,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       const int nkb = nmain + (t.split == 0 ? p.nk2 : 0);
       // snake: every other round of this CTA walks K backwards, starting where the data it
       // (and its neighbours) just streamed is still in L2
-      const bool rev = p.snake && (((u - group) / ngroups) & 1);
+      const bool rev = p.snake && (it & 1);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -444,7 +449,10 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
     // --------------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int it = 0;
-    for (int u = group; u < g.total_units; u += ngroups, ++it) {
+    int st_it = 0;  // EPI = 3: TMA stores issued by this warp
+    for (;; ++it) {
+      const int u = group + it * ngroups;
+      if (u >= g.total_units) break;
       const Unit t = decode_unit(g, u);
       const Prob& p = g.p[t.prob];
       const int m0 = t.m_blk * (kBM * CG) + rank * kBM;
@@ -452,78 +460,81 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int row = (g.dbg == 3) ? 0x7fffffff : m0 + q * 32 + lane;
-      // W + A·B (K = r is tiny, so the epilogue is the whole cost): fetch this row's
-      // 256-column segment of W before waiting for the accumulator, all 32 loads in flight.
-      const bool add256 = WADD && p.out_mode == OUT_BF16_ADD && p.bn == 256 && BN_MAX == 256;
-      uint4 cin[WADD ? 32 : 1];
-      if (add256) {
-        const __nv_bfloat16* src = p.Cin + (long long)row * p.ldc + n0;
-#pragma unroll
-        for (int e = 0; e < 32; ++e)
-          cin[e] = (row < p.M && n0 + 8 * e < p.N) ? __ldg(reinterpret_cast<const uint4*>(src) + e) : make_uint4(0, 0, 0, 0);
-      }
-      if constexpr (EPI == 2) mbar_wait(&ct_full[acc], acc_phase);  // Cin block of this tile landed
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN_MAX;
       if (g.dbg == 4) {
-      } else if (EPI == 2) {
-        const int lr = q * 32 + lane;  // local output row
+      } else if (EPI == 3) {
+        // bf16 tile -> per-warp swizzled smem staging -> TMA store (coalesced full-line
+        // writes; rows >= M / cols >= N are clipped by the tensor map bounds).
+        uint8_t* stg = smem + STAGES * C::STAGE_BYTES + q * 4096;
+        const uint32_t sw = (uint32_t)(lane >> 1) & 3u;  // 64B swizzle: 16B chunk ^= row bits [1,3)
 #pragma unroll 1
         for (int c = 0; c < p.bn; c += 32) {
           if (n0 + c >= p.N) break;  // warp-uniform
           uint32_t v[32];
           tmem_ld_32x32b_x32(t_row + c, v);
           tmem_ld_wait();
-          if (row < p.M) {
-            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.D) + (long long)row * p.ldd + n0 + c;
+          const int buf = st_it & 1;
+          if (st_it >= 2) {
+            if (lane == 0) bulk_wait_read<1>();  // the store that last used `buf` has read it
+            __syncwarp();
+          }
+          uint8_t* rowp = stg + buf * 2048 + lane * 64;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              if (n0 + c + 8 * e < p.N) {
-                float f[8];
+          for (int e = 0; e < 4; ++e) {
+            uint4 o;
+            o.x = pack_bf16x2(__uint_as_float(v[8 * e + 0]), __uint_as_float(v[8 * e + 1]));
+            o.y = pack_bf16x2(__uint_as_float(v[8 * e + 2]), __uint_as_float(v[8 * e + 3]));
+            o.z = pack_bf16x2(__uint_as_float(v[8 * e + 4]), __uint_as_float(v[8 * e + 5]));
+            o.w = pack_bf16x2(__uint_as_float(v[8 * e + 6]), __uint_as_float(v[8 * e + 7]));
+            *reinterpret_cast<uint4*>(rowp + ((e ^ sw) << 4)) = o;
+          }
+          fence_proxy_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tm.m[t.prob][4], stg + buf * 2048, n0 + c, m0 + q * 32);
+            bulk_commit();
+          }
+          ++st_it;
+        }
+      } else if (p.out_mode == OUT_F32_FOLD) {
+        // sum of the fold column blocks (w = fold_w in {8, 16, 32}), in block order
+        float o[32];
 #pragma unroll
-                for (int x = 0; x < 8; ++x)
-                  f[x] = __uint_as_float(v[8 * e + x]) +
-                         __bfloat162float(sCt[acc * BN_MAX * kBM + (c + 8 * e + x) * kBM + lr]);
-                uint4 o;
-                o.x = pack_bf16x2(f[0], f[1]);
-                o.y = pack_bf16x2(f[2], f[3]);
-                o.z = pack_bf16x2(f[4], f[5]);
-                o.w = pack_bf16x2(f[6], f[7]);
-                *reinterpret_cast<uint4*>(dst + 8 * e) = o;
-              }
+        for (int x = 0; x < 32; ++x) o[x] = 0.f;
+        const int w = p.fold_w;
+#pragma unroll 1
+        for (int c = 0; c < p.bn; c += 32) {
+          uint32_t v[32];
+          const bool full32 = p.bn - c >= 32;
+          if (full32) tmem_ld_32x32b_x32(t_row + c, v);
+          else tmem_ld_32x32b_x16(t_row + c, v);
+          tmem_ld_wait();
+          if (w == 32) {
+#pragma unroll
+            for (int x = 0; x < 32; ++x) o[x] += __uint_as_float(v[x]);
+          } else if (w == 16) {
+#pragma unroll
+            for (int x = 0; x < 16; ++x) o[x] += __uint_as_float(v[x]);
+            if (full32) {
+#pragma unroll
+              for (int x = 0; x < 16; ++x) o[x] += __uint_as_float(v[16 + x]);
+            }
+          } else {
+#pragma unroll
+            for (int b8 = 0; b8 < 4; ++b8) {
+              if (b8 >= 2 && !full32) break;
+#pragma unroll
+              for (int x = 0; x < 8; ++x) o[x] += __uint_as_float(v[8 * b8 + x]);
             }
           }
         }
-      } else if (add256) {
+        if (row < p.M) {
+          float* dst = static_cast<float*>(p.D) + t.split * p.split_stride + (long long)row * p.ldd;
 #pragma unroll
-        for (int c8 = 0; c8 < 8; ++c8) {
-          if (n0 + c8 * 32 >= p.N) break;  // warp-uniform
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(t_row + c8 * 32, v);
-          tmem_ld_wait();
-          if (row < p.M) {
-            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.D) + (long long)row * p.ldd + n0 + c8 * 32;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              if (n0 + c8 * 32 + 8 * e < p.N) {
-                const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&cin[c8 * 4 + e]);
-                float f[8];
-#pragma unroll
-                for (int x = 0; x < 4; ++x) {
-                  const float2 cf = __bfloat1622float2(c2[x]);
-                  f[2 * x] = __uint_as_float(v[8 * e + 2 * x]) + cf.x;
-                  f[2 * x + 1] = __uint_as_float(v[8 * e + 2 * x + 1]) + cf.y;
-                }
-                uint4 o;
-                o.x = pack_bf16x2(f[0], f[1]);
-                o.y = pack_bf16x2(f[2], f[3]);
-                o.z = pack_bf16x2(f[4], f[5]);
-                o.w = pack_bf16x2(f[6], f[7]);
-                *reinterpret_cast<uint4*>(dst + 8 * e) = o;
-              }
-            }
-          }
+          for (int e = 0; e < 8; ++e)
+            if (4 * e < w) *reinterpret_cast<float4*>(dst + 4 * e) = make_float4(o[4 * e], o[4 * e + 1], o[4 * e + 2], o[4 * e + 3]);
         }
       } else if (p.bn % 32 == 0) {
 #pragma unroll 1
@@ -547,15 +558,12 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote<CG>(&tempty[acc], 0);  // leader's barrier
-      if constexpr (EPI == 2) {
-        if (lane == 0) mbar_arrive(&ct_empty[acc]);  // Cin block buffer free
-      }
       if (p.counters) splitk_fixup(p, t, m0, n0, row, s_flag);
-      if (p.pub_flags) {  // this tile's rows are stored: publish for dependent problems
-        __threadfence();
-        epi_bar();
-        if (threadIdx.x == 4 * 32) st_release_gpu(p.pub_flags + t.m_blk, (int)p.epoch);
-      }
+      if (g.trace && threadIdx.x == 4 * 32) g.trace[8 * u + 3] = globaltimer();
+    }
+    if constexpr (EPI == 3) {
+      if (lane == 0) bulk_wait_all();  // stores complete before the CTA retires
+      __syncwarp();
     }
   }
   tc_fence_before();
