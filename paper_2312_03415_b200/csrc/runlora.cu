@@ -318,6 +318,7 @@ Skinny job_dB_dense(const runlora_shape_t& s, const void* z2d, const void* A, vo
 struct ZPlan {
   bool ok;
   int sz, kpz[2];        // projection K-splits (Z1, Z2 alike) and k-blocks per split
+  int szf, kpzf;         // forward1's Z2 = X·A alone: its K-split and k-blocks per split
   int bn_z[2];           // MMA N of the projections
   int bn_t;              // MMA N of the reductions (sz * r when the partials are folded)
   int tsplits, kpt;      // token-reduction splits and k-blocks (64 tokens) per split
@@ -353,6 +354,18 @@ ZPlan plan_z(const runlora_shape_t& s) {
   }
   if (const char* e = getenv("RUNLORA_ZSPLIT")) sz = std::max(1, atoi(e));
   f.sz = sz;
+  // forward1 runs Z2 alone (mt row tiles): the same rule with half the tiles
+  int szf = 1;
+  if ((r == 8 || r == 16 || r == 32) && mt < 148) {
+    for (int c = 2; c <= 8 && mt * c <= 2 * 148; c *= 2) {
+      if (c * r > 64) break;
+      const int64_t kp = (kbz[1] + c - 1) / c;
+      if ((kbz[1] + kp - 1) / kp != c) break;
+      szf = c;
+    }
+  }
+  f.szf = szf;
+  f.kpzf = (int)((kbz[1] + szf - 1) / szf);
   for (int i = 0; i < 2; ++i) {
     f.kpz[i] = (int)((kbz[i] + sz - 1) / sz);
     if ((kbz[i] + f.kpz[i] - 1) / f.kpz[i] != sz) return f;
@@ -399,28 +412,31 @@ size_t partial_need(const runlora_shape_t& s) {
 
 // ------------------------------------------------------------ workspace layout
 struct Layout {
-  size_t z1, z2, arep, wp, p, total;
+  size_t z1, z2, arep, brep, wp, p, total;
 };
 
 // Z1, Z2: n x r (or n x sz*r partial blocks, see ZPlan); arep: A repeated sz times along its
-// columns (k x sz*r, the dX concat tail against Z1's partial blocks).
+// columns (k x sz*r, backward1's dX tail against Z1's blocks); brep: B stacked sz times
+// (sz*r x m, forward1's Y tail against Z2's blocks).
 Layout layout_of(const runlora_shape_t& s) {
   const size_t es = s.dtype == RUNLORA_BF16 ? 2 : 4;
   const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
   const ZPlan f = plan_z(s);
-  const size_t zc = (size_t)r * (f.ok ? f.sz : 1);
+  const size_t zc = (size_t)r * (f.ok ? f.sz : 1);                       // Z1 (and backward Z2)
+  const size_t zc2 = (size_t)r * (f.ok ? std::max(f.sz, f.szf) : 1);    // Z2 (forward1 too)
   Layout L;
   L.z1 = 0;
   L.z2 = al((size_t)n * zc * es);
-  L.arep = L.z2 + al((size_t)n * zc * es);
-  L.wp = L.arep + (f.ok && f.sz > 1 ? al((size_t)k * zc * es) : 0);
+  L.arep = L.z2 + al((size_t)n * zc2 * es);
+  L.brep = L.arep + (f.ok && f.sz > 1 ? al((size_t)k * zc * es) : 0);
+  L.wp = L.brep + (f.ok && f.szf > 1 ? al((size_t)m * r * f.szf * es) : 0);
   L.p = L.wp + al((size_t)k * m * es);
   L.total = L.p + (s.dtype == RUNLORA_BF16 ? partial_need(s) : 0);
   return L;
 }
 
 struct Bufs {
-  void *z1, *z2, *arep, *wp;
+  void *z1, *z2, *arep, *brep, *wp;
   float* P;
 };
 
@@ -437,6 +453,7 @@ runlora_status_t bind_ws(const runlora_shape_t& s, void* ws, size_t ws_bytes, Bu
   b->z1 = base + L.z1;
   b->z2 = base + L.z2;
   b->arep = base + L.arep;
+  b->brep = base + L.brep;
   b->wp = base + L.wp;
   b->P = reinterpret_cast<float*>(base + L.p);
   return RUNLORA_OK;
@@ -521,12 +538,43 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
   q.ldd = m;
   if (v == 1) {
     // Z2 = X·A (never saved for the backward), then Y = [X | Z2]·[W ; B]
-    Skinny j = job_Z2(s, X, A, b.z2);
-    RL_TRY(run_skinny(c, &j, 1, b.P, KID_GEMM_PROJ, st));
     q.b = mat(W, k, m);
-    q.a2 = mat(b.z2, n, r);
-    q.b2 = mat(B, r, m);
-    q.K2 = (int)r;
+    const ZPlan f = plan_z(s);
+    if (f.ok && f.szf > 1) {
+      // Z2 as szf K-split bf16 blocks (every CTA slot streams X, no reducer), then
+      // Y = [X | Z2_0 | .. | Z2_{szf-1}]·[W ; B ; .. ; B] (B stacked szf times, side stream)
+      const int zc = (int)(r * f.szf);
+      cudaStream_t ss = c.side_stream();
+      cudaEventRecord(c.fork_event(), st);
+      cudaStreamWaitEvent(ss, c.fork_event(), 0);
+      cudaError_t e = launch_repeat_cols(c, B, 1, (int)(r * m), f.szf, b.brep, ss);
+      if (e != cudaSuccess) return cuda_fail(e, "repeat_cols launch");
+      cudaEventRecord(c.join_event(), ss);
+      GemmReq z = base_req((int)n, (int)r, KID_GEMM_PROJ);
+      z.a = mat(X, n, k);
+      z.b = mat(A, k, r);
+      z.b_mn = true;
+      z.K1 = (int)k;
+      z.BN = f.bn_z[1];
+      z.a_stream_once = true;
+      z.out_mode = OUT_BF16;
+      z.D = b.z2;
+      z.ldd = zc;
+      z.split_stride = r;
+      z.splits = f.szf;
+      z.kb_per_split = f.kpzf;
+      RL_TRY(gemm(c, z, st));
+      cudaStreamWaitEvent(st, c.join_event(), 0);
+      q.a2 = mat(b.z2, n, zc);
+      q.b2 = mat(b.brep, zc, m);
+      q.K2 = zc;
+    } else {
+      Skinny j = job_Z2(s, X, A, b.z2);
+      RL_TRY(run_skinny(c, &j, 1, b.P, KID_GEMM_PROJ, st));
+      q.a2 = mat(b.z2, n, r);
+      q.b2 = mat(B, r, m);
+      q.K2 = (int)r;
+    }
   } else {
     RL_TRY(wprime_t_bf16(c, s, W, A, B, b.wp, st));  // W'ᵀ [m, k]
     q.b = mat(b.wp, m, k);
