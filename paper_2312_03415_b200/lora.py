@@ -20,11 +20,27 @@ def _shape(X, W, A):
     return rl.make_shape(n, k, m, r, X.dtype)
 
 
+class GradSink:
+    """fp32 destination of one linear's adapter gradients (views dA [k, r], dB [r, m], e.g.
+    into a data-parallel bucket): the backward accumulates into them (micro-batching,
+    SURVEY §8(e) "C5") instead of returning A.grad / B.grad, then calls ``on_ready``."""
+
+    def __init__(self, dA: torch.Tensor, dB: torch.Tensor, on_ready=None):
+        self.dA, self.dB, self.on_ready = dA, dB, on_ready
+        self.accumulate = False  # set True after the first micro-batch of a step
+
+    def ready(self):
+        self.accumulate = True
+        if self.on_ready is not None:
+            self.on_ready(self)
+
+
 class LoRALinearFunction(torch.autograd.Function):
-    """Y = LoRA(X) with forward variant plan.fwd and backward variant plan.bwd."""
+    """Y = LoRA(X) with forward variant plan.fwd and backward variant plan.bwd.
+    With a GradSink the adapter gradients go to the sink (fp32) and A.grad/B.grad stay None."""
 
     @staticmethod
-    def forward(ctx, X, W, A, B, fwd: int, bwd: int):
+    def forward(ctx, X, W, A, B, fwd: int, bwd: int, sink: GradSink | None = None):
         for t, name in ((X, "X"), (W, "W"), (A, "A"), (B, "B")):
             if not t.is_cuda or not t.is_contiguous():
                 raise ValueError(f"{name} must be a contiguous CUDA tensor")
@@ -34,6 +50,7 @@ class LoRALinearFunction(torch.autograd.Function):
         h.forward(fwd, shape, X, W, A, B, Y)
         ctx.save_for_backward(X, W, A, B)   # no XA
         ctx.bwd = bwd
+        ctx.sink = sink
         ctx.need_dx = ctx.needs_input_grad[0]
         return Y
 
@@ -43,12 +60,17 @@ class LoRALinearFunction(torch.autograd.Function):
         dY = dY.contiguous()
         shape = _shape(X, W, A)
         h = rl.handle(X.device)
+        dX = torch.empty_like(X) if ctx.need_dx else None
+        sink = ctx.sink
+        if sink is not None:
+            h.backward(ctx.bwd, shape, X, W, A, B, dY, dX, sink.dA, sink.dB, accumulate=sink.accumulate)
+            sink.ready()
+            return dX, None, None, None, None, None, None
         gdt = torch.float32 if X.dtype == torch.float32 else A.dtype
         dA = torch.empty(A.shape, dtype=gdt, device=X.device)
         dB = torch.empty(B.shape, dtype=gdt, device=X.device)
-        dX = torch.empty_like(X) if ctx.need_dx else None
         h.backward(ctx.bwd, shape, X, W, A, B, dY, dX, dA, dB)
-        return dX, None, dA.to(A.dtype), dB.to(B.dtype), None, None
+        return dX, None, dA.to(A.dtype), dB.to(B.dtype), None, None, None
 
 
 def lora_linear(X, W, A, B, plan=None, criterion=rl.BY_FLOPS):

@@ -73,6 +73,40 @@ C4 = {(r, n): case(f"C4_opt_r{r}_n{n}", 4, 3 * ri + ni, n, 2048, 2048, r, "bf16"
 
 ALL_CONFIGS = [C1, *C2.values(), C3_UP, C3_DOWN, *C4.values()]
 
+# --- C5: stack of LoRA-adapted linears with Llama-7B projection shapes -------------
+# Per layer (reading R15): q, k, v, o: d -> d; gate, up: d -> f; down: f -> d.
+C5_LINEARS = ("q", "k", "v", "o", "gate", "up", "down")
+C5_D, C5_F, C5_R = 4096, 11008, 16
+
+
+def c5_dims(name: str, d: int = C5_D, f: int = C5_F):
+    """(in, out) of linear ``name`` in a layer of width d and MLP width f."""
+    return {"gate": (d, f), "up": (d, f), "down": (f, d)}.get(name, (d, d))
+
+
+def c5_linear(layer: int, name: str, n: int, d: int = C5_D, f: int = C5_F, r: int = C5_R, dtype: str = "bf16"):
+    """The Case of one linear of the stack; seeds [2312, 5, layer*8 + index, t]."""
+    k, m = c5_dims(name, d, f)
+    return case(f"C5_L{layer}_{name}", 5, layer * 8 + C5_LINEARS.index(name), n, k, m, r, dtype)
+
+
+def c5_weights(layers: int, n: int, d: int = C5_D, f: int = C5_F, r: int = C5_R, dtype: str = "bf16"):
+    """[{name: {"W", "A", "B"}}] per layer (CPU tensors), same law as C2/C3 (Var 1/k, 1/r)."""
+    out = []
+    for layer in range(layers):
+        lw = {}
+        for name in C5_LINEARS:
+            c = c5_linear(layer, name, n, d, f, r, dtype)
+            lw[name] = {"W": draw(c, T_W, (c.k, c.m)), "A": draw(c, T_A, (c.k, c.r)), "B": draw(c, T_B, (c.r, c.m))}
+        out.append(lw)
+    return out
+
+
+def c5_io(n: int, d: int = C5_D, dtype: str = "bf16"):
+    """Stack input X [n, d] ~ N(0, 1) and the synthetic output gradient dY [n, d] ~ N(0, 1)."""
+    c = case("C5_io", 5, 1000, n, d, d, 1, dtype)
+    return draw(c, T_X, (n, d)), draw(c, T_DY, (n, d))
+
 
 def draw(c: Case, t: int, shape) -> torch.Tensor:
     """Draw tensor ``t`` of case ``c``; returns a CPU torch tensor in c's dtype."""
