@@ -27,7 +27,9 @@ runlora_status_t runlora_debug_gemm(runlora_handle_t h, int M, int N, int K1, co
                                     void* D, const void* Cin, int BN, int splits, int cg, void* stream);
 /* Debug timeline of the last launch of kernel id RUNLORA_TRACE (env, read at handle creation):
  * 8 uint64 per unit {producer start, dependencies met, last load issued, epilogue done (ns),
- * CTA index, problem index}.  Returns the number of units copied (0 if tracing is off). */
+ * CTA index, problem index}; with max_units = 65536 the host buffer must hold 8*65536 + 4*1024 words:
+ * 4 per CTA follow the unit records {kernel entry, inputs ready (after the PDL wait), exit}.
+ * Returns the number of units copied (0 if tracing is off). */
 int runlora_debug_trace(runlora_handle_t h, unsigned long long* host, int max_units);
 #ifdef __cplusplus
 }

@@ -40,7 +40,7 @@ Ctx::Ctx(int device) : device_(device) {
   if (const char* e = getenv("RUNLORA_TMA_STORE_WPRIME")) tma_store_wprime_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_TRACE")) {
     trace_kid = atoi(e);
-    if (cudaMalloc(&trace, sizeof(unsigned long long) * 8 * kTraceUnits) != cudaSuccess) trace = nullptr;
+    if (cudaMalloc(&trace, sizeof(unsigned long long) * (8 * kTraceUnits + 4 * 1024)) != cudaSuccess) trace = nullptr;
   }
   {
     std::vector<uint16_t> eye(128 * 128, 0);

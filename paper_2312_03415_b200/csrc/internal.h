@@ -91,7 +91,7 @@ class Ctx {
   // debug timeline buffer (env RUNLORA_TRACE=<kernel id>): see GemmArgs::trace
   unsigned long long* trace = nullptr;
   int trace_kid = -1;
-  static constexpr int kTraceUnits = 1 << 16;
+  static constexpr int kTraceUnits = 1 << 16;  // == kTraceMaxUnits (tc_gemm.cuh); + 4 words per CTA
   bool tma_store_main() const { return tma_store_main_; }
   bool tma_store_wprime() const { return tma_store_wprime_; }
 

@@ -287,9 +287,9 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
       tm.m[q][2] = tm.m[q][0];
       tm.m[q][3] = tm.m[q][1];
     }
-    if (r.tma_store) {  // D: box {32 columns, 32 rows}, 64B swizzle (one epilogue warp's chunk)
+    if (r.tma_store) {  // D: box {64 columns, 32 rows}, 128B swizzle (one epilogue warp's chunk)
       const DeviceMat dm{r.D, (int64_t)r.M, (int64_t)r.N, r.ldd};
-      if (!ctx.tmap(dm, 32, &tm.m[q][4], err, 64)) return cudaErrorInvalidValue;
+      if (!ctx.tmap(dm, 32, &tm.m[q][4], err, 128)) return cudaErrorInvalidValue;
     }
     Prob& p = g.p[q];
     p.M = r.M;

@@ -1225,5 +1225,9 @@ extern "C" int runlora_debug_trace(runlora_handle_t h, unsigned long long* host,
   DeviceGuard dg(h->ctx->device());
   if (cudaMemcpy(host, h->ctx->trace, sizeof(unsigned long long) * 8 * n, cudaMemcpyDeviceToHost) != cudaSuccess)
     return 0;
+  if (n == Ctx::kTraceUnits &&  // full buffer requested: the per-CTA records follow
+      cudaMemcpy(host + 8ull * n, h->ctx->trace + 8ull * n, sizeof(unsigned long long) * 4 * 1024,
+                 cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 0;
   return n;
 }

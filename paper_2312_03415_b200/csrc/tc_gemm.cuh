@@ -81,6 +81,7 @@ struct Prob {
 };
 
 constexpr int kMaxProb = 4;
+constexpr int kTraceMaxUnits = 1 << 16;  // debug trace: unit records, then 4 words per CTA
 
 struct GemmArgs {
   Prob p[kMaxProb];
@@ -96,6 +97,7 @@ struct Tmaps {  // per problem: A1, B1, A2, B2, D (EPI = 3: TMA-store epilogue)
   CUtensorMap m[kMaxProb][5];
 };
 
+constexpr int kStgBufs = 4;  // EPI = 3 staging tiles per epilogue warp (a 256-wide tile's 4 stores never wait)
 constexpr int kBM = 128;  // rows per CTA
 constexpr int kBK = 64;
 constexpr int kGemmThreads = 256;
@@ -107,8 +109,8 @@ struct TileCfg {
   static constexpr uint32_t A_BYTES = kBM * kBK * 2;
   static constexpr uint32_t B_BYTES = (BN_MAX / CG) * kBK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  // EPI = 3: per epilogue warp two 32-row x 32-column bf16 staging tiles (64B swizzle) for TMA stores
-  static constexpr uint32_t STG_BYTES = EPI == 3 ? 4 * 2 * 2048 : 0;
+  // EPI = 3: per epilogue warp kStgBufs 32-row x 64-column bf16 staging tiles (128B swizzle)
+  static constexpr uint32_t STG_BYTES = EPI == 3 ? 4 * kStgBufs * 4096 : 0;
   // up to ~225 KB of the 227 KB opt-in smem per SM (7 stages for the 256x256 pair tiles)
   static constexpr int STAGES_RAW = ((OCC == 1 ? 225 : 110) * 1024 - STG_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
@@ -299,6 +301,9 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
   const int group = blockIdx.x / CG;
   const int ngroups = gridDim.x / CG;
 
+  // debug timeline per CTA (after the units): {kernel entry, inputs ready (after PDL wait), exit}
+  unsigned long long* ctrace = g.trace ? g.trace + 8ull * kTraceMaxUnits + 4ull * blockIdx.x : nullptr;
+  if (ctrace && threadIdx.x == 0) ctrace[0] = globaltimer();
   if (warp == 0 && lane == 0) {
     for (int q = 0; q < g.nprob; ++q)
       for (int j = 0; j < 4; ++j)
@@ -324,6 +329,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
   // everything above overlapped the previous kernel's tail (PDL); inputs are read below
   pdl_wait();
   pdl_launch_dependents();
+  if (ctrace && threadIdx.x == 0) ctrace[1] = globaltimer();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -466,34 +472,39 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       if (g.dbg == 4) {
       } else if (EPI == 3) {
         // bf16 tile -> per-warp swizzled smem staging -> TMA store (coalesced full-line
-        // writes; rows >= M / cols >= N are clipped by the tensor map bounds).
-        uint8_t* stg = smem + STAGES * C::STAGE_BYTES + q * 4096;
-        const uint32_t sw = (uint32_t)(lane >> 1) & 3u;  // 64B swizzle: 16B chunk ^= row bits [1,3)
+        // writes; rows >= M / cols >= N are clipped by the tensor map bounds).  64-column
+        // chunks, kStgBufs staging tiles per warp: a buffer is reused only after the store
+        // issued kStgBufs chunks earlier has finished reading it.
+        uint8_t* stg = smem + STAGES * C::STAGE_BYTES + q * (kStgBufs * 4096);
+        const uint32_t sw = (uint32_t)lane & 7u;  // 128B swizzle: 16B chunk ^= row bits [0,3)
 #pragma unroll 1
-        for (int c = 0; c < p.bn; c += 32) {
+        for (int c = 0; c < p.bn; c += 64) {
           if (n0 + c >= p.N) break;  // warp-uniform
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(t_row + c, v);
-          tmem_ld_wait();
-          const int buf = st_it & 1;
-          if (st_it >= 2) {
-            if (lane == 0) bulk_wait_read<1>();  // the store that last used `buf` has read it
+          const int buf = st_it % kStgBufs;
+          if (st_it >= kStgBufs) {
+            if (lane == 0) bulk_wait_read<kStgBufs - 1>();
             __syncwarp();
           }
-          uint8_t* rowp = stg + buf * 2048 + lane * 64;
+          uint8_t* rowp = stg + buf * 4096 + lane * 128;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            uint4 o;
-            o.x = pack_bf16x2(__uint_as_float(v[8 * e + 0]), __uint_as_float(v[8 * e + 1]));
-            o.y = pack_bf16x2(__uint_as_float(v[8 * e + 2]), __uint_as_float(v[8 * e + 3]));
-            o.z = pack_bf16x2(__uint_as_float(v[8 * e + 4]), __uint_as_float(v[8 * e + 5]));
-            o.w = pack_bf16x2(__uint_as_float(v[8 * e + 6]), __uint_as_float(v[8 * e + 7]));
-            *reinterpret_cast<uint4*>(rowp + ((e ^ sw) << 4)) = o;
+          for (int hf = 0; hf < 2; ++hf) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(t_row + c + 32 * hf, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              uint4 o;
+              o.x = pack_bf16x2(__uint_as_float(v[8 * e + 0]), __uint_as_float(v[8 * e + 1]));
+              o.y = pack_bf16x2(__uint_as_float(v[8 * e + 2]), __uint_as_float(v[8 * e + 3]));
+              o.z = pack_bf16x2(__uint_as_float(v[8 * e + 4]), __uint_as_float(v[8 * e + 5]));
+              o.w = pack_bf16x2(__uint_as_float(v[8 * e + 6]), __uint_as_float(v[8 * e + 7]));
+              *reinterpret_cast<uint4*>(rowp + (((4 * hf + e) ^ sw) << 4)) = o;
+            }
           }
           fence_proxy_async_shared();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tm.m[t.prob][4], stg + buf * 2048, n0 + c, m0 + q * 32);
+            tma_store_2d(&tm.m[t.prob][4], stg + buf * 4096, n0 + c, m0 + q * 32);
             bulk_commit();
           }
           ++st_it;
@@ -573,6 +584,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
   }
+  if (ctrace && threadIdx.x == 64) ctrace[2] = globaltimer();
 }
 
 }  // namespace runlora

@@ -36,13 +36,21 @@ for _ in range(a.steps):
 torch.cuda.synchronize()
 lib = rl._lib
 lib.runlora_debug_trace.restype = C.c_int
-buf = np.zeros(8 * 65536, dtype=np.uint64)
+buf = np.zeros(8 * 65536 + 4 * 1024, dtype=np.uint64)
 n = lib.runlora_debug_trace(h._h, buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), 65536)
+cta = buf[8 * 65536:].reshape(1024, 4).astype(np.int64)
 t = buf[: 8 * n].reshape(n, 8).astype(np.int64)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 T = (t[:, :4] - t0) / 1e3  # us
 print(f"units {len(t)}  span {T[:, 3].max():.1f} us  CTAs {len(np.unique(t[:, 4]))}")
+ct = cta[cta[:, 0] > 0]
+if len(ct):
+    k0 = ct[:, 0].min()
+    print(f"kernel: CTA entry {0:.1f}..{(ct[:, 0].max() - k0) / 1e3:.1f} us, inputs ready "
+          f"{(ct[:, 1].min() - k0) / 1e3:.1f}..{(ct[:, 1].max() - k0) / 1e3:.1f}, first unit {(t0 - k0) / 1e3:.1f}, "
+          f"last unit done {(t[:, 3].max() - k0) / 1e3:.1f}, CTA exit {(ct[:, 2].min() - k0) / 1e3:.1f}.."
+          f"{(ct[:, 2].max() - k0) / 1e3:.1f} us")
 for q in np.unique(t[:, 5]):
     s = t[:, 5] == q
     wait = T[s, 1] - T[s, 0]
