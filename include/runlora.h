@@ -33,9 +33,16 @@
  *
  * Dtypes: RUNLORA_F32 computes every product in true fp32 FFMA (no TF32);
  * RUNLORA_BF16 reads bf16 operands, accumulates in fp32 on the tcgen05 tensor
- * cores and stores Y, dX and the rank-r intermediates in bf16; W+AB is formed in
- * fp32 and rounded once (R10).  For bf16, k, m and r must be multiples
- * of 8 (TMA needs 16-byte row strides) — otherwise RUNLORA_ERR_ALIGNMENT.
+ * cores and stores Y, dX and the rank-r intermediates in bf16 (X·A and dY·Bᵀ as
+ * one block per K-split, summed in fp32 by the tensor cores where they are used,
+ * DESIGN.md R16); W+AB is formed in fp32 and rounded once (R10).  For
+ * bf16, k, m and r must be multiples of 8 (TMA needs 16-byte row strides) —
+ * otherwise RUNLORA_ERR_ALIGNMENT.
+ *
+ * Concurrency: a handle may be driven from ONE host thread at a time.  Calls for
+ * different streams may be interleaved from that thread if every stream uses its
+ * own workspace (the handle's internal side stream orders the small side kernels
+ * of all calls in host-call order).  Use one handle per host thread otherwise.
  *
  * Errors: a non-zero runlora_status_t; runlora_last_error() returns a
  * thread-local message naming the offending argument(s).  No C++ exception
@@ -132,8 +139,9 @@ runlora_status_t runlora_workspace_size(const runlora_shape_t* s, int fwd, int b
  * RUNLORA_BY_FLOPS: argmin of Table 1 over {F1,F2} and {B1..B5}, ties to the
  *   lowest index ("with flops criterion").  `ops`, workspace, stream unused.
  * RUNLORA_BY_TIME: every executable candidate is run on `ops` on `stream`
- *   (3 warm-ups, 15 timed reps each, CUDA events, median); forward and backward
- *   timed independently; argmin of the medians.  Needs a workspace of
+ *   (3 warm-up rounds, 15 timed rounds, candidates interleaved; one rep = 4
+ *   back-to-back calls between CUDA events; median); forward and backward timed
+ *   independently; argmin of the medians (within 1 %: fewer FLOPs wins).  Needs a workspace of
  *   runlora_workspace_size(s, 2, 4) bytes or more (the largest candidate set).
  *   Blocks the calling thread until timing is done.
  * RUNLORA_HYBRID: as TIME but only candidates within 2x of the FLOP minimum.
@@ -160,9 +168,10 @@ runlora_status_t runlora_backward(runlora_handle_t h, int bwd, const runlora_sha
                                   int accumulate, void* workspace, size_t ws_bytes, void* stream);
 
 /* Split backward for data-parallel overlap: _params computes dA, dB (and, for
- * backward1..3, leaves Z1 = dY·Bᵀ in the workspace); _input computes dX and must
- * follow the _params call of the same variant/shape with the same workspace on
- * the same stream.  runlora_backward == _params then _input. */
+ * backward1..3, leaves Z1 = dY·Bᵀ — and for backward1 A repeated per Z1 block —
+ * in the workspace); _input computes dX and must follow the _params call of the
+ * same variant/shape with the same workspace on the same stream (for backward4/5
+ * _input is self-contained).  runlora_backward == _params then _input. */
 runlora_status_t runlora_backward_params(runlora_handle_t h, int bwd, const runlora_shape_t* s,
                                          const void* X, const void* W, const void* A, const void* B,
                                          const void* dY, void* dA, void* dB, int grad_dtype, int accumulate,

@@ -1020,8 +1020,11 @@ runlora_status_t runlora_select(runlora_handle_t h, const runlora_shape_t* s, in
   if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
     return fail(RUNLORA_ERR_TIMING, "cudaEventCreate failed");
   // Candidates are timed round-robin (one rep of each per round) so that clock and power
-  // drift under the 1 kW cap affects all of them alike; median of 15 rounds after 3.
-  const int warm = 3, reps = 15;
+  // drift under the 1 kW cap affects all of them alike; median of 15 rounds after 3.  A rep
+  // is `inner` back-to-back calls between two events (their mean): a single call timed from
+  // an idle GPU is dominated by launch latency at small shapes and misranks candidates
+  // whose steady-state cost is lower.
+  const int warm = 3, reps = 15, inner = 4;
   const uint64_t fmin = std::min(p.flops_fwd[1], p.flops_fwd[2]);
   uint64_t bmin = p.flops_bwd[1];
   for (int v = 2; v <= 5; ++v) bmin = std::min(bmin, p.flops_bwd[v]);
@@ -1036,11 +1039,13 @@ runlora_status_t runlora_select(runlora_handle_t h, const runlora_shape_t* s, in
     for (size_t ci = 0; ci < cands.size() && st_all == RUNLORA_OK; ++ci) {
       const int v = cands[ci];
       cudaEventRecord(e0, st);
-      if (v < 10)
-        st_all = do_forward(h, v, s, ops->X, ops->W, ops->A, ops->B, ops->Y, ws, ws_bytes, stream);
-      else
-        st_all = do_backward(h, v - 10, s, ops->X, ops->W, ops->A, ops->B, ops->dY, ops->dX, ops->dA, ops->dB,
-                             ops->grad_dtype, 0, ws, ws_bytes, stream);
+      for (int j = 0; j < inner && st_all == RUNLORA_OK; ++j) {
+        if (v < 10)
+          st_all = do_forward(h, v, s, ops->X, ops->W, ops->A, ops->B, ops->Y, ws, ws_bytes, stream);
+        else
+          st_all = do_backward(h, v - 10, s, ops->X, ops->W, ops->A, ops->B, ops->dY, ops->dX, ops->dA, ops->dB,
+                               ops->grad_dtype, 0, ws, ws_bytes, stream);
+      }
       cudaEventRecord(e1, st);
       if (st_all != RUNLORA_OK) break;
       if (cudaEventSynchronize(e1) != cudaSuccess) {
@@ -1049,7 +1054,7 @@ runlora_status_t runlora_select(runlora_handle_t h, const runlora_shape_t* s, in
       }
       float ms = 0.f;
       cudaEventElapsedTime(&ms, e0, e1);
-      if (i >= warm) times[ci].push_back(ms * 1000.f);
+      if (i >= warm) times[ci].push_back(ms * 1000.f / inner);
     }
   }
   if (st_all == RUNLORA_OK) {

@@ -72,10 +72,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--only", default=None)
+    ap.add_argument("--per-rank", type=int, default=1,
+                    help="divide n by P: one rank's share of a token-sharded run (C4 at P ranks)")
     a = ap.parse_args()
     cfgs = [c for c in synth.ALL_CONFIGS if c.dtype == "bf16"]
     if a.only:
         cfgs = [c for c in cfgs if c.name.startswith(a.only)]
+    if a.per_rank > 1:
+        cfgs = [synth.case(f"{c.name}_P{a.per_rank}", c.cfg, c.sub, c.n // a.per_rank, c.k, c.m, c.r, c.dtype)
+                for c in cfgs]
     for c in cfgs:
         print(json.dumps(run(c, a.steps)), flush=True)
         torch.cuda.empty_cache()
