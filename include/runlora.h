@@ -41,8 +41,9 @@
  *
  * Concurrency: a handle may be driven from ONE host thread at a time.  Calls for
  * different streams may be interleaved from that thread if every stream uses its
- * own workspace (the handle's internal side stream orders the small side kernels
- * of all calls in host-call order).  Use one handle per host thread otherwise.
+ * own workspace.  Every launch of a call goes to the caller's stream (one
+ * programmatic-dependent-launch chain, no internal streams or events).  Use one
+ * handle per host thread otherwise.
  *
  * Errors: a non-zero runlora_status_t; runlora_last_error() returns a
  * thread-local message naming the offending argument(s).  No C++ exception

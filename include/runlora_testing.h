@@ -31,6 +31,12 @@ runlora_status_t runlora_debug_gemm(runlora_handle_t h, int M, int N, int K1, co
  * 4 per CTA follow the unit records {kernel entry, inputs ready (after the PDL wait), exit}.
  * Returns the number of units copied (0 if tracing is off). */
 int runlora_debug_trace(runlora_handle_t h, unsigned long long* host, int max_units);
+/* Launch timeline (env RUNLORA_LTRACE=1 at handle creation): 8 uint64 per launch since the
+ * last read {min CTA entry, min ready (after the PDL wait), max ready, min exit, max exit,
+ * 0, 0, 0} (%globaltimer ns) and the launch's kernel id in kids[]; resets the record and
+ * synchronises the device.  Returns the number of launches copied. */
+int runlora_debug_ltrace(runlora_handle_t h, unsigned long long* host, int* kids, int max_launches);
+const char* runlora_debug_kernel_name(int kid);
 #ifdef __cplusplus
 }
 #endif

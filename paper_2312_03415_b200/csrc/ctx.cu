@@ -1,5 +1,6 @@
 // Per-handle host context: device facts, TMA descriptor cache, launch counting
 // and CUDA-event kernel profiling.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -28,6 +29,13 @@ Ctx::Ctx(int device) : device_(device) {
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
+  if (const char* e = getenv("RUNLORA_LTRACE"); e && atoi(e) != 0) {
+    std::vector<unsigned long long> init((size_t)kLTraceSlots * 8, 0ull);
+    for (int i = 0; i < kLTraceSlots; ++i) init[8 * i] = init[8 * i + 1] = init[8 * i + 3] = ~0ull;
+    if (cudaMalloc(&ltrace_, init.size() * 8) != cudaSuccess ||
+        cudaMemcpy(ltrace_, init.data(), init.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+      ltrace_ = nullptr;
+  }
   if (cudaMalloc(&counters_, sizeof(int) * kCounterCap) == cudaSuccess) {
     if (cudaMemset(counters_, 0, sizeof(int) * kCounterCap) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
       cudaFree(counters_);
@@ -49,6 +57,7 @@ Ctx::Ctx(int device) : device_(device) {
         cudaMemcpy(identity_, eye.data(), eye.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess) {
       if (identity_) cudaFree(identity_);
   if (trace) cudaFree(trace);
+  if (ltrace_) cudaFree(ltrace_);
       identity_ = nullptr;
     }
   }
@@ -65,27 +74,7 @@ Ctx::~Ctx() {
   if (counters_) cudaFree(counters_);
   if (identity_) cudaFree(identity_);
   if (trace) cudaFree(trace);
-  if (side_) cudaStreamDestroy(side_);
-  if (ev_fork_) cudaEventDestroy(ev_fork_);
-  if (ev_join_) cudaEventDestroy(ev_join_);
-  if (ev_arep_) cudaEventDestroy(ev_arep_);
-}
-
-cudaStream_t Ctx::side_stream() {
-  if (!side_) cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking);
-  return side_;
-}
-cudaEvent_t Ctx::fork_event() {
-  if (!ev_fork_) cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming);
-  return ev_fork_;
-}
-cudaEvent_t Ctx::arep_event() {
-  if (!ev_arep_) cudaEventCreateWithFlags(&ev_arep_, cudaEventDisableTiming);
-  return ev_arep_;
-}
-cudaEvent_t Ctx::join_event() {
-  if (!ev_join_) cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming);
-  return ev_join_;
+  if (ltrace_) cudaFree(ltrace_);
 }
 
 bool Ctx::tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* err, int swz, int chunks) {
@@ -141,6 +130,27 @@ bool Ctx::tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* 
   tmaps_[key] = tm;
   *out = tm;
   return true;
+}
+
+unsigned long long* Ctx::ltrace_slot(KernelId kid) {
+  if (!ltrace_ || ltrace_next_ >= kLTraceSlots) return nullptr;
+  ltrace_kid_.push_back((int)kid);
+  return ltrace_ + 8ull * (ltrace_next_++);
+}
+
+int Ctx::ltrace_read(unsigned long long* host, int* kids, int max_slots) {
+  if (!ltrace_) return 0;
+  const int n = std::min(max_slots, ltrace_next_);
+  if (cudaDeviceSynchronize() != cudaSuccess ||
+      cudaMemcpy(host, ltrace_, 8ull * 8 * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 0;
+  for (int i = 0; i < n; ++i) kids[i] = ltrace_kid_[i];
+  std::vector<unsigned long long> init((size_t)kLTraceSlots * 8, 0ull);  // reset for the next window
+  for (int i = 0; i < kLTraceSlots; ++i) init[8 * i] = init[8 * i + 1] = init[8 * i + 3] = ~0ull;
+  cudaMemcpy(ltrace_, init.data(), init.size() * 8, cudaMemcpyHostToDevice);
+  ltrace_next_ = 0;
+  ltrace_kid_.clear();
+  return n;
 }
 
 cudaEvent_t Ctx::get_event() {

@@ -67,6 +67,18 @@ struct GemmReq {
   bool tma_store;  // OUT_BF16 through the TMA-store epilogue (all problems of a launch alike)
 };
 
+struct ReduceJob {
+  const float* P;
+  int splits;
+  int64_t split_stride;
+  int rows, cols;
+  int64_t ldp;
+  void* out;
+  int out_bf16;
+  int64_t ldo;
+  int transpose, accumulate;
+};
+
 class Ctx {
  public:
   explicit Ctx(int device);
@@ -80,16 +92,15 @@ class Ctx {
   bool fixup_enabled() const { return counters_ != nullptr && fixup_; }
   bool occ2() const { return occ2_; }  // 2 CTAs/SM for rank-r kernels (env RUNLORA_OCC2=0 disables)
   bool pdl() const { return pdl_; }    // programmatic dependent launch (env RUNLORA_PDL=0 disables)
-  // Side stream for small work that can overlap the next big GEMM (fork/join by events).
-  cudaStream_t side_stream();
-  cudaEvent_t fork_event();
-  cudaEvent_t join_event();
-  cudaEvent_t arep_event();  // A repeated for backward1's dX tail is ready (side stream)
-  bool join_pending = false;
+  // split-K reductions of a backward whose launch waits until after its dX GEMM (same stream)
+  std::vector<ReduceJob> deferred_reduce;
   // 128x128 bf16 identity (device): A operand of the block-diagonal tail that adds W in W + A·B
   const void* identity() const { return identity_; }
   // debug timeline buffer (env RUNLORA_TRACE=<kernel id>): see GemmArgs::trace
   unsigned long long* trace = nullptr;
+  unsigned long long* ltrace_ = nullptr;
+  int ltrace_next_ = 0;
+  std::vector<int> ltrace_kid_;
   int trace_kid = -1;
   static constexpr int kTraceUnits = 1 << 16;  // == kTraceMaxUnits (tc_gemm.cuh); + 4 words per CTA
   bool tma_store_main() const { return tma_store_main_; }
@@ -101,6 +112,13 @@ class Ctx {
   // {swz/2, box_rows, chunks} -> one TMA op fills `chunks` adjacent swizzle columns.
   bool tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* err, int swz_bytes = 128,
             int chunks = 0);
+
+  // Launch timeline (env RUNLORA_LTRACE=1): each launch gets a device slot of 8 words
+  // {min CTA entry, min ready, max ready, min exit, max exit} (%globaltimer ns; "ready" =
+  // after the PDL wait), filled by atomics from every CTA; see runlora_debug_ltrace.
+  static constexpr int kLTraceSlots = 4096;
+  unsigned long long* ltrace_slot(KernelId kid);
+  int ltrace_read(unsigned long long* host, int* kids, int max_slots);
 
   // Profiling hooks around every launch.
   void launch_begin(cudaStream_t s, KernelId kid);
@@ -120,8 +138,6 @@ class Ctx {
   void* identity_ = nullptr;
   bool tma_store_main_ = false;   // env RUNLORA_TMA_STORE_MAIN=1
   bool tma_store_wprime_ = true;  // env RUNLORA_TMA_STORE_WPRIME=0
-  cudaStream_t side_ = nullptr;
-  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_arep_ = nullptr;
   bool fixup_ = false;     // env RUNLORA_SPLITK_FIXUP=1: in-kernel fix-up instead of the reducer launch
   bool occ2_ = true;
   bool pdl_ = true;
@@ -148,17 +164,7 @@ class Ctx {
 cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t s, std::string* err);
 // Fixed-order sum of fp32 split-K slabs P[split][rows][ldp] (first `cols` columns) into
 // out (fp32 or bf16; optionally transposed: out[j*ldo + i]; optionally accumulated).
-struct ReduceJob {
-  const float* P;
-  int splits;
-  int64_t split_stride;
-  int rows, cols;
-  int64_t ldp;
-  void* out;
-  int out_bf16;
-  int64_t ldo;
-  int transpose, accumulate;
-};
+
 cudaError_t launch_splitk_reduce(Ctx& ctx, const ReduceJob* jobs, int njobs, cudaStream_t s);
 // dst[i, t*cols + j] = src[i, j] for t < reps (bf16, row-major; 16-byte column groups).
 cudaError_t launch_repeat_cols(Ctx& ctx, const void* src, int rows, int cols, int reps, void* dst, cudaStream_t s);

@@ -122,14 +122,17 @@ cudaError_t dispatch_tc(Ctx& ctx, int bn_max, int cg, bool occ2, bool tma_store,
 struct ReduceArgs {
   ReduceJob j[2];
   long long total0, total;
+  unsigned long long* ltrace;
 };
 
 // One thread per (row i, 4-column group): float4 loads of every split slab in fixed
 // split order (deterministic), 4 slabs in flight at a time.  Column groups vary fastest
 // so a warp reads contiguous 512 B of each slab.
 __global__ void __launch_bounds__(256, 4) splitk_reduce_kernel(const __grid_constant__ ReduceArgs a) {
+  if (threadIdx.x == 0) ltrace_mark(a.ltrace, 0);
   pdl_wait();
   pdl_launch_dependents();
+  if (threadIdx.x == 0) ltrace_mark(a.ltrace, 1);
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < a.total;
        idx += (long long)gridDim.x * blockDim.x) {
     const bool second = idx >= a.total0;
@@ -173,13 +176,16 @@ __global__ void __launch_bounds__(256, 4) splitk_reduce_kernel(const __grid_cons
       }
     }
   }
+  if (threadIdx.x == 0) ltrace_mark(a.ltrace, 2);
 }
 
 // ------------------------------------------------------------ column repeat
 __global__ void __launch_bounds__(256) repeat_cols_kernel(const uint4* __restrict__ src, int rows, int g, int reps,
-                                                          uint4* __restrict__ dst) {
+                                                          uint4* __restrict__ dst, unsigned long long* lt) {
+  if (threadIdx.x == 0) ltrace_mark(lt, 0);
   pdl_wait();
   pdl_launch_dependents();
+  if (threadIdx.x == 0) ltrace_mark(lt, 1);
   const long long total = (long long)rows * g * reps;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -187,6 +193,7 @@ __global__ void __launch_bounds__(256) repeat_cols_kernel(const uint4* __restric
     const int c = (int)(idx % g);
     dst[idx] = src[i * g + c];
   }
+  if (threadIdx.x == 0) ltrace_mark(lt, 2);
 }
 
 // ------------------------------------------------------------ fp32 SIMT GEMM
@@ -345,6 +352,7 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
   }
   g.nprob = nreq;
   g.trace = (ctx.trace && ctx.trace_kid == reqs[0].kid && g.total_units <= Ctx::kTraceUnits) ? ctx.trace : nullptr;
+  g.ltrace = ctx.ltrace_slot(reqs[0].kid);
   if (const char* d = getenv("RUNLORA_DBG_GEMM")) g.dbg = atoi(d);
   for (int q = nreq; q < kMaxProb; ++q) g.p[q] = g.p[0], g.p[q].units = 0;
   if (g.total_units <= 0) return cudaSuccess;
@@ -369,6 +377,7 @@ cudaError_t launch_splitk_reduce(Ctx& ctx, const ReduceJob* jobs, int njobs, cud
   long long blocks = (a.total + 255) / 256;
   const long long cap = (long long)ctx.num_sms() * 16;
   if (blocks > cap) blocks = cap;
+  a.ltrace = ctx.ltrace_slot(KID_SPLITK_REDUCE);
   ctx.launch_begin(s, KID_SPLITK_REDUCE);
   cudaError_t e = launch_pdl(ctx, splitk_reduce_kernel, dim3((unsigned)blocks), dim3(256), s, a);
   ctx.launch_end(s);
@@ -383,7 +392,8 @@ cudaError_t launch_repeat_cols(Ctx& ctx, const void* src, int rows, int cols, in
   if (blocks > ctx.num_sms() * 8LL) blocks = ctx.num_sms() * 8LL;
   ctx.launch_begin(s, KID_REPEAT_COLS);
   cudaError_t e = launch_pdl(ctx, repeat_cols_kernel, dim3((unsigned)blocks), dim3(256), s,
-                             static_cast<const uint4*>(src), rows, g, reps, static_cast<uint4*>(dst));
+                             static_cast<const uint4*>(src), rows, g, reps, static_cast<uint4*>(dst),
+                             ctx.ltrace_slot(KID_REPEAT_COLS));
   ctx.launch_end(s);
   return e;
 }

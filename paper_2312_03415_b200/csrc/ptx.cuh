@@ -19,6 +19,21 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// Launch timeline slot (Ctx::ltrace_slot): phase 0 = CTA entry, 1 = ready (after the PDL
+// wait), 2 = CTA exit.  Called by one thread per CTA.
+__device__ __forceinline__ void ltrace_mark(unsigned long long* lt, int phase) {
+  if (!lt) return;
+  const unsigned long long t = globaltimer();
+  if (phase == 0) {
+    atomicMin(lt + 0, t);
+  } else if (phase == 1) {
+    atomicMin(lt + 1, t);
+    atomicMax(lt + 2, t);
+  } else {
+    atomicMin(lt + 3, t);
+    atomicMax(lt + 4, t);
+  }
+}
 
 // ------------------------------------------- programmatic dependent launch
 // wait: block until the preceding grid in the stream has completed and its memory is

@@ -214,9 +214,10 @@ GemmReq base_req(int M, int N, KernelId kid) {
   return q;
 }
 
-// defer_reduce: run the reducer on the handle's side stream (forked from `st` by an event)
-// so that it overlaps whatever the caller enqueues next on `st`; the caller must join
-// (cudaStreamWaitEvent(st, c.join_event())) before the outputs are consumed.
+// defer_reduce: the reducer is not launched here but stashed in the context; the caller
+// (do_backward) launches it on the same stream right after the dX GEMM, where it
+// co-resides with that GEMM's tail in the programmatic-dependent-launch chain (a side
+// stream joined by events breaks the chain: measured 5-7 µs per event wait).
 runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, KernelId kid, cudaStream_t st,
                             bool defer_reduce = false) {
   const SkinnyPlan p = plan_skinny(jobs, n);
@@ -268,18 +269,12 @@ runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, KernelI
   cudaError_t e = launch_tc_gemm(c, q, n, st, &err);
   if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
   if (!p.direct && !fixup) {
-    cudaStream_t rs = st;
     if (defer_reduce) {
-      rs = c.side_stream();
-      cudaEventRecord(c.fork_event(), st);
-      cudaStreamWaitEvent(rs, c.fork_event(), 0);
+      c.deferred_reduce.assign(rj, rj + n);
+      return RUNLORA_OK;
     }
-    e = launch_splitk_reduce(c, rj, n, rs);
+    e = launch_splitk_reduce(c, rj, n, st);
     if (e != cudaSuccess) return cuda_fail(e, "splitk_reduce launch");
-    if (defer_reduce) {
-      cudaEventRecord(c.join_event(), rs);
-      c.join_pending = true;
-    }
   }
   return RUNLORA_OK;
 }
@@ -544,12 +539,8 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
       // Z2 as szf K-split bf16 blocks (every CTA slot streams X, no reducer), then
       // Y = [X | Z2_0 | .. | Z2_{szf-1}]·[W ; B ; .. ; B] (B stacked szf times, side stream)
       const int zc = (int)(r * f.szf);
-      cudaStream_t ss = c.side_stream();
-      cudaEventRecord(c.fork_event(), st);
-      cudaStreamWaitEvent(ss, c.fork_event(), 0);
-      cudaError_t e = launch_repeat_cols(c, B, 1, (int)(r * m), f.szf, b.brep, ss);
+      cudaError_t e = launch_repeat_cols(c, B, 1, (int)(r * m), f.szf, b.brep, st);
       if (e != cudaSuccess) return cuda_fail(e, "repeat_cols launch");
-      cudaEventRecord(c.join_event(), ss);
       GemmReq z = base_req((int)n, (int)r, KID_GEMM_PROJ);
       z.a = mat(X, n, k);
       z.b = mat(A, k, r);
@@ -564,7 +555,6 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
       z.splits = f.szf;
       z.kb_per_split = f.kpzf;
       RL_TRY(gemm(c, z, st));
-      cudaStreamWaitEvent(st, c.join_event(), 0);
       q.a2 = mat(b.z2, n, zc);
       q.b2 = mat(b.brep, zc, m);
       q.K2 = zc;
@@ -591,13 +581,9 @@ runlora_status_t grads_tok_bf16(Ctx& c, int v, const ZPlan& f, const runlora_sha
   const int zc = (int)(r * f.sz);  // columns of the partial-Z matrices
   std::string err;
   if (v == 1 && f.sz > 1) {
-    // A repeated sz times for backward1's dX tail, on the side stream under the projections
-    cudaStream_t ss = c.side_stream();
-    cudaEventRecord(c.fork_event(), st);
-    cudaStreamWaitEvent(ss, c.fork_event(), 0);
-    cudaError_t e = launch_repeat_cols(c, A, (int)k, (int)r, f.sz, b.arep, ss);
+    // A repeated sz times for backward1's dX tail (2 µs; in the same PDL chain)
+    cudaError_t e = launch_repeat_cols(c, A, (int)k, (int)r, f.sz, b.arep, st);
     if (e != cudaSuccess) return cuda_fail(e, "repeat_cols launch");
-    cudaEventRecord(c.arep_event(), ss);
   }
   // projections: Zp[:, s*r:(s+1)*r] = K-split s of dY·Bᵀ / X·A (bf16)
   GemmReq q[2];
@@ -656,18 +642,12 @@ runlora_status_t grads_tok_bf16(Ctx& c, int v, const ZPlan& f, const runlora_sha
   }
   e = launch_tc_gemm(c, q, 2, st, &err);
   if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
-  cudaStream_t rs = st;
-  if (defer) {
-    rs = c.side_stream();
-    cudaEventRecord(c.fork_event(), st);
-    cudaStreamWaitEvent(rs, c.fork_event(), 0);
+  if (defer) {  // launched by do_backward right after the dX GEMM
+    c.deferred_reduce.assign(rj, rj + 2);
+    return RUNLORA_OK;
   }
-  e = launch_splitk_reduce(c, rj, 2, rs);
+  e = launch_splitk_reduce(c, rj, 2, st);
   if (e != cudaSuccess) return cuda_fail(e, "splitk_reduce launch");
-  if (defer) {
-    cudaEventRecord(c.join_event(), rs);
-    c.join_pending = true;
-  }
   return RUNLORA_OK;
 }
 
@@ -730,7 +710,6 @@ runlora_status_t input_bf16(Ctx& c, int v, const runlora_shape_t& s, const void*
       // backward1's adapter-gradient pass left Z1 as sz partial blocks: dY·Wᵀ + Σ_s Z1_s·Aᵀ =
       // [dY | Z1_0 | .. | Z1_{sz-1}]·[Wᵀ ; Aᵀ ; .. ; Aᵀ]
       const int zc = (int)(r * f.sz);
-      cudaStreamWaitEvent(st, c.arep_event(), 0);  // A_rep, built by backward_params
       q.a2 = mat(b.z1, n, zc);
       q.b2 = mat(b.arep, k, zc);
       q.K2 = zc;
@@ -880,17 +859,21 @@ runlora_status_t do_input(runlora_handle_t h, int bwd, const runlora_shape_t* s,
 runlora_status_t do_backward(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X, const void* W,
                              const void* A, const void* B, const void* dY, void* dX, void* dA, void* dB,
                              int grad_dtype, int accumulate, void* ws, size_t ws_bytes, void* stream) {
-  // The adapter-gradient reducer runs on the side stream, overlapping the dX GEMM; the
-  // caller's stream joins it before this call's work is complete in stream order.
+  // With dX, the adapter-gradient reducer is launched after the dX GEMM on the same stream:
+  // it co-resides with the GEMM's last wave and the whole backward stays one
+  // programmatic-dependent-launch chain (no cross-stream events).
   const bool defer = dX != nullptr;
-  h->ctx->join_pending = false;
+  h->ctx->deferred_reduce.clear();
   runlora_status_t st = do_params(h, bwd, s, X, W, A, B, dY, dA, dB, grad_dtype, accumulate, ws, ws_bytes, stream,
                                   defer);
   if (st == RUNLORA_OK && dX) st = do_input(h, bwd, s, W, A, B, dY, dX, ws, ws_bytes, stream);
-  if (h->ctx->join_pending) {
+  if (!h->ctx->deferred_reduce.empty()) {
+    // launched even if dX failed, so dA/dB are complete whenever the call reports success
     DeviceGuard dg(h->ctx->device());
-    cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), h->ctx->join_event(), 0);
-    h->ctx->join_pending = false;
+    cudaError_t e = launch_splitk_reduce(*h->ctx, h->ctx->deferred_reduce.data(),
+                                         (int)h->ctx->deferred_reduce.size(), static_cast<cudaStream_t>(stream));
+    h->ctx->deferred_reduce.clear();
+    if (e != cudaSuccess && st == RUNLORA_OK) st = cuda_fail(e, "splitk_reduce launch");
   }
   return st;
 }
@@ -1235,4 +1218,18 @@ extern "C" int runlora_debug_trace(runlora_handle_t h, unsigned long long* host,
                  cudaMemcpyDeviceToHost) != cudaSuccess)
     return 0;
   return n;
+}
+
+// Launch timeline (env RUNLORA_LTRACE=1 at handle creation): copies the records of the
+// launches since the last read — 8 uint64 per launch {min CTA entry, min ready, max ready,
+// min exit, max exit, 0, 0, 0} (%globaltimer ns) and the kernel id of each — then resets.
+// Synchronises the device.  Returns the number of launches copied.
+extern "C" int runlora_debug_ltrace(runlora_handle_t h, unsigned long long* host, int* kids, int max_launches) {
+  if (!h || !h->ctx || !host || !kids) return 0;
+  DeviceGuard dg(h->ctx->device());
+  return h->ctx->ltrace_read(host, kids, max_launches);
+}
+
+extern "C" const char* runlora_debug_kernel_name(int kid) {
+  return (kid >= 0 && kid < KID_COUNT) ? kKernelNames[kid] : "?";
 }

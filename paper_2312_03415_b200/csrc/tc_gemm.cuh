@@ -91,6 +91,7 @@ struct GemmArgs {
   // Debug timeline (RUNLORA_TRACE): per unit u, trace[8u + {0: producer start, 2: last load
   // issued, 3: epilogue done, 4: CTA, 5: problem}] (%globaltimer ns).
   unsigned long long* trace;
+  unsigned long long* ltrace;  // launch timeline slot (nullptr: off)
 };
 
 struct Tmaps {  // per problem: A1, B1, A2, B2, D (EPI = 3: TMA-store epilogue)
@@ -304,6 +305,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
   // debug timeline per CTA (after the units): {kernel entry, inputs ready (after PDL wait), exit}
   unsigned long long* ctrace = g.trace ? g.trace + 8ull * kTraceMaxUnits + 4ull * blockIdx.x : nullptr;
   if (ctrace && threadIdx.x == 0) ctrace[0] = globaltimer();
+  if (threadIdx.x == 0) ltrace_mark(g.ltrace, 0);
   if (warp == 0 && lane == 0) {
     for (int q = 0; q < g.nprob; ++q)
       for (int j = 0; j < 4; ++j)
@@ -330,6 +332,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
   pdl_wait();
   pdl_launch_dependents();
   if (ctrace && threadIdx.x == 0) ctrace[1] = globaltimer();
+  if (threadIdx.x == 0) ltrace_mark(g.ltrace, 1);
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -585,6 +588,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
     tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
   }
   if (ctrace && threadIdx.x == 64) ctrace[2] = globaltimer();
+  if (threadIdx.x == 64) ltrace_mark(g.ltrace, 2);
 }
 
 }  // namespace runlora
