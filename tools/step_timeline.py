@@ -27,9 +27,13 @@ def main():
     ap.add_argument("--plan", default="2,1")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--show", type=int, default=2)
+    ap.add_argument("--shape", default=None, help="n,k,m (default: C2, n=8192, k=m=4096)")
     a = ap.parse_args()
     assert os.environ.get("RUNLORA_LTRACE"), "set RUNLORA_LTRACE=1"
     c = synth.C2[a.r]
+    if a.shape:
+        n, k, m = (int(x) for x in a.shape.split(","))
+        c = synth.case(f"adhoc_{n}_{k}_{m}_{a.r}", 0, 77, n, k, m, a.r, "bf16")
     d = {k: v.cuda() for k, v in synth.operands(c).items()}
     h = rl.handle(0)
     lib = rl._lib
