@@ -78,9 +78,7 @@ Ctx::~Ctx() {
 }
 
 bool Ctx::tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* err, int swz, int chunks) {
-  char key[160];
-  snprintf(key, sizeof key, "%p/%lld/%lld/%lld/%d/%d/%d", m.ptr, (long long)m.rows, (long long)m.cols,
-           (long long)m.ld, box_rows, swz, chunks);
+  const TmapKey key{m.ptr, m.rows, m.cols, m.ld, box_rows, swz, chunks};
   {
     std::lock_guard<std::mutex> g(tmap_mu_);
     auto it = tmaps_.find(key);

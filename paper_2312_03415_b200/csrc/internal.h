@@ -143,8 +143,25 @@ class Ctx {
   bool pdl_ = true;
   CUtensorMapL2promotion promo_mn_ = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;  // 3-D (MN-major) boxes       // env RUNLORA_OCC2=0: one CTA per SM for the rank-r kernels too
   void* encode_fn_ = nullptr;
+  struct TmapKey {
+    const void* ptr;
+    int64_t rows, cols, ld;
+    int box_rows, swz, chunks;
+    bool operator==(const TmapKey& o) const {
+      return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && box_rows == o.box_rows &&
+             swz == o.swz && chunks == o.chunks;
+    }
+  };
+  struct TmapKeyHash {
+    size_t operator()(const TmapKey& k) const {
+      size_t h = std::hash<const void*>()(k.ptr);
+      for (int64_t v : {k.rows, k.cols, k.ld, (int64_t)k.box_rows, (int64_t)k.swz, (int64_t)k.chunks})
+        h = h * 1000003u ^ std::hash<int64_t>()(v);
+      return h;
+    }
+  };
   std::mutex tmap_mu_;
-  std::unordered_map<std::string, CUtensorMap> tmaps_;
+  std::unordered_map<TmapKey, CUtensorMap, TmapKeyHash> tmaps_;
   bool profiling_ = false;
   uint64_t launches_ = 0;
   struct Pending {

@@ -367,6 +367,9 @@ ZPlan plan_z(const runlora_shape_t& s) {
   }
   f.bn_t = sz > 1 ? (int)(sz * r) : skinny_bn(r, true);
   if (r > f.bn_t || f.bn_t > 256) return f;
+  // without K-split blocks the projections need enough row tiles to stream from every SM;
+  // otherwise the fp32 split-K path (run_skinny + reducer) is the better plan
+  if (sz == 1 && 3 * 2 * mt < 2 * 148) return f;
   // token splits: as many as fit in one wave of CTA slots
   const int64_t tiles = (k + kBM - 1) / kBM + (m + kBM - 1) / kBM;
   int64_t ts = std::max<int64_t>(1, (2 * 148) / tiles);
@@ -381,7 +384,6 @@ ZPlan plan_z(const runlora_shape_t& s) {
   off += al((size_t)f.tsplits * (size_t)m * w * 4);
   f.bytes = off;
   f.ok = true;
-  (void)mt;
   return f;
 }
 
@@ -406,8 +408,31 @@ size_t partial_need(const runlora_shape_t& s) {
 }
 
 // ------------------------------------------------------------ workspace layout
+// Split-K plan of a main GEMM with fewer 256x256 tiles than CTA pairs (small n: the
+// K loop of a lone tile is latency-bound): splits so that the units fill about one wave
+// of pairs, fp32 slabs [split][M][N], summed in fixed order into bf16 by the reducer.
+struct MainSplit {
+  int splits, kps;
+};
+MainSplit main_split(int64_t M, int64_t N, int64_t K) {
+  const int64_t units = ((M + 255) / 256) * ((N + 255) / 256);
+  const int64_t nkb = (K + kBK - 1) / kBK;
+  MainSplit ms{1, (int)nkb};
+  if (units >= 74 || nkb < 8) return ms;
+  int64_t sp = std::min<int64_t>({74 / units, 8, nkb / 4});
+  if (sp < 2) return ms;
+  ms.kps = (int)((nkb + sp - 1) / sp);
+  ms.splits = (int)((nkb + ms.kps - 1) / ms.kps);
+  return ms;
+}
+size_t main_split_bytes(const runlora_shape_t& s) {
+  const MainSplit a = main_split(s.n, s.m, s.k), b = main_split(s.n, s.k, s.m);
+  return std::max(a.splits > 1 ? al((size_t)a.splits * s.n * s.m * 4) : 0,
+                  b.splits > 1 ? al((size_t)b.splits * s.n * s.k * 4) : 0);
+}
+
 struct Layout {
-  size_t z1, z2, arep, brep, wp, p, total;
+  size_t z1, z2, arep, brep, wp, p, pm, total;
 };
 
 // Z1, Z2: n x r (or n x sz*r partial blocks, see ZPlan); arep: A repeated sz times along its
@@ -426,13 +451,15 @@ Layout layout_of(const runlora_shape_t& s) {
   L.brep = L.arep + (f.ok && f.sz > 1 ? al((size_t)k * zc * es) : 0);
   L.wp = L.brep + (f.ok && f.szf > 1 ? al((size_t)m * r * f.szf * es) : 0);
   L.p = L.wp + al((size_t)k * m * es);
-  L.total = L.p + (s.dtype == RUNLORA_BF16 ? partial_need(s) : 0);
+  L.pm = L.p + (s.dtype == RUNLORA_BF16 ? partial_need(s) : 0);  // main-GEMM split-K slabs after
+  L.total = L.pm + (s.dtype == RUNLORA_BF16 ? main_split_bytes(s) : 0);  // the rank-r ones (see main_gemm)
   return L;
 }
 
 struct Bufs {
   void *z1, *z2, *arep, *brep, *wp;
-  float* P;
+  float* P;   // rank-r split-K slabs (may still await the deferred reducer during the dX GEMM)
+  float* Pm;  // main-GEMM split-K slabs
 };
 
 runlora_status_t bind_ws(const runlora_shape_t& s, void* ws, size_t ws_bytes, Bufs* b) {
@@ -451,6 +478,7 @@ runlora_status_t bind_ws(const runlora_shape_t& s, void* ws, size_t ws_bytes, Bu
   b->brep = base + L.brep;
   b->wp = base + L.wp;
   b->P = reinterpret_cast<float*>(base + L.p);
+  b->Pm = reinterpret_cast<float*>(base + L.pm);
   return RUNLORA_OK;
 }
 
@@ -508,6 +536,27 @@ runlora_status_t wprime_t_bf16(Ctx& c, const runlora_shape_t& s, const void* W, 
   q.BN = 256;
   q.tma_store = c.tma_store_wprime();
   return gemm(c, q, st);
+}
+
+// Runs a main GEMM (bf16 D = q.D, ld q.ldd), split over K into fp32 slabs in the P region
+// and reduced when main_split says so.
+runlora_status_t main_gemm(Ctx& c, GemmReq q, Bufs& b, cudaStream_t st) {
+  const MainSplit ms = main_split(q.M, q.N, q.K1);
+  if (ms.splits <= 1) return gemm(c, q, st);
+  void* out = q.D;
+  const int64_t ldo = q.ldd;
+  q.out_mode = OUT_F32;
+  q.tma_store = false;
+  q.D = b.Pm;
+  q.ldd = q.N;
+  q.split_stride = (int64_t)q.M * q.N;
+  q.splits = ms.splits;
+  q.kb_per_split = ms.kps;
+  RL_TRY(gemm(c, q, st));
+  ReduceJob rj{b.Pm, ms.splits, (int64_t)q.M * q.N, q.M, q.N, q.N, out, 1, ldo, 0, 0};
+  cudaError_t e = launch_splitk_reduce(c, &rj, 1, st);
+  if (e != cudaSuccess) return cuda_fail(e, "splitk_reduce launch");
+  return RUNLORA_OK;
 }
 
 // The dominant Y / dX GEMMs: 256x256 tiles on CTA pairs (cta_group::2) unless disabled.
@@ -570,7 +619,7 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
     q.b = mat(b.wp, m, k);
     q.b_mn = false;
   }
-  return gemm(c, q, st);
+  return main_gemm(c, q, b, st);
 }
 
 // backward1/5 adapter gradients: projections launch, reductions launch, reducer (see ZPlan).
@@ -718,7 +767,7 @@ runlora_status_t input_bf16(Ctx& c, int v, const runlora_shape_t& s, const void*
     RL_TRY(wprime_bf16(c, s, W, A, B, b.wp, st));
     q.b = mat(b.wp, k, m);
   }
-  return gemm(c, q, st);
+  return main_gemm(c, q, b, st);
 }
 
 // ------------------------------------------------------------ fp32 variants

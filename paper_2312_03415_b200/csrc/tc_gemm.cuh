@@ -80,7 +80,7 @@ struct Prob {
   int tail_diag;
 };
 
-constexpr int kMaxProb = 4;
+constexpr int kMaxProb = 2;  // problems per launch (dual launches); kernel params stay ~1.8 KB
 constexpr int kTraceMaxUnits = 1 << 16;  // debug trace: unit records, then 4 words per CTA
 
 struct GemmArgs {

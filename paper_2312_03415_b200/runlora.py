@@ -154,11 +154,17 @@ def select_by_flops(shape: Shape) -> Plan:
 
 
 def _ptr(t):
-    return None if t is None else C.c_void_p(t.data_ptr())
+    # argtypes declare c_void_p: a plain int (or None) converts without a wrapper object
+    return None if t is None else t.data_ptr()
+
+
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
 
 
 def _stream(device):
-    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+    if _raw_stream is not None:
+        return _raw_stream(device.index or 0)
+    return torch.cuda.current_stream(device).cuda_stream
 
 
 class Handle:
