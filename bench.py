@@ -138,6 +138,30 @@ def run_reference(args):
     return 0
 
 
+def _launch_work(h, rl, step, steps):
+    """Median in-step work time (µs) per library kernel name over `steps` steps, from the
+    library's launch records (RUNLORA_LTRACE): last CTA exit - first CTA ready."""
+    import ctypes as C
+    lib = rl._lib
+    if not hasattr(lib, "runlora_debug_ltrace"):
+        return {}
+    lib.runlora_debug_ltrace.restype = C.c_int
+    lib.runlora_debug_kernel_name.restype = C.c_char_p
+    buf = np.zeros(8 * 4096, dtype=np.uint64)
+    kids = np.zeros(4096, dtype=np.int32)
+    args = (h._h, buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), kids.ctypes.data_as(C.POINTER(C.c_int)), 4096)
+    lib.runlora_debug_ltrace(*args)  # reset
+    for _ in range(steps):
+        step()
+    n = lib.runlora_debug_ltrace(*args)
+    rec = buf[: 8 * n].reshape(n, 8).astype(np.int64)
+    out = {}
+    for i in range(n):
+        if rec[i, 4] > 0 and rec[i, 1] > 0:
+            out.setdefault(lib.runlora_debug_kernel_name(int(kids[i])).decode(), []).append((rec[i, 4] - rec[i, 1]) / 1e3)
+    return {k: float(np.median(v)) for k, v in out.items()}
+
+
 def cpu_baseline(c, fwd, bwd, target_s=12.0, slice_tokens=1024):
     """The oracle timed on the host cores on a bounded sample (rank 0, N=1 only): the
     selected pair on consecutive 1024-token slices of the workload (cycling), until
@@ -186,6 +210,9 @@ def main():
         return run_reference(args)
 
     import torch.distributed as dist
+    # per-launch records (first/last CTA ready and exit): the in-step work time of each
+    # kernel, reported beside the CUDA-event durations (read over a window of steps below)
+    os.environ.setdefault("RUNLORA_LTRACE", "1")
     from paper_2312_03415_b200 import runlora as rl
     from paper_2312_03415_b200 import dp
 
@@ -326,6 +353,16 @@ def main():
         gbs = bytes_step / (ms_tot / args.steps * 1e-3) / 1e9
         hbm_roof[nm] = {"bound": "hbm", "bytes_per_step": bytes_step, "achieved": gbs, "peak": hbm,
                         "unit": "GB/s", "frac": gbs / hbm, "peak_source": f"of {peak_src}: HBM copy bandwidth"}
+    # in-step work time per launch (first CTA ready after the PDL wait -> last CTA exit)
+    work = _launch_work(h, rl, step, min(args.steps, 40))
+    for nm, r_ in hbm_roof.items():
+        if nm in work:
+            per_launch = r_["bytes_per_step"] / max(1.0, round(prof[nm][0] / args.steps))
+            r_["work_us_per_launch"] = work[nm]
+            r_["achieved_work"] = per_launch / (work[nm] * 1e-6) / 1e9
+            r_["frac_work"] = r_["achieved_work"] / hbm
+    if "gemm_main" in work:
+        roof["work_us_per_launch"] = work["gemm_main"]
     roof["hbm_kernels"] = hbm_roof
 
     # ---------------- end to end through the C ABI with host buffers
