@@ -22,7 +22,6 @@ Ctx::Ctx(int device) : device_(device) {
       q == cudaDriverEntryPointSuccess)
     encode_fn_ = fn;
   if (const char* e = getenv("RUNLORA_MAIN_CG")) main_cg_ = atoi(e) == 1 ? 1 : 2;
-  if (const char* e = getenv("RUNLORA_SPLITK_FIXUP")) fixup_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_OCC2")) occ2_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_PDL")) pdl_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_L2PROMO_MN")) promo_mn_ = (CUtensorMapL2promotion)atoi(e);
@@ -36,16 +35,6 @@ Ctx::Ctx(int device) : device_(device) {
         cudaMemcpy(ltrace_, init.data(), init.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
       ltrace_ = nullptr;
   }
-  if (cudaMalloc(&counters_, sizeof(int) * kCounterCap) == cudaSuccess) {
-    if (cudaMemset(counters_, 0, sizeof(int) * kCounterCap) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
-      cudaFree(counters_);
-      counters_ = nullptr;
-    }
-  } else {
-    counters_ = nullptr;
-  }
-  if (const char* e = getenv("RUNLORA_TMA_STORE_MAIN")) tma_store_main_ = atoi(e) != 0;
-  if (const char* e = getenv("RUNLORA_TMA_STORE_WPRIME")) tma_store_wprime_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_TRACE")) {
     trace_kid = atoi(e);
     if (cudaMalloc(&trace, sizeof(unsigned long long) * (8 * kTraceUnits + 4 * 1024)) != cudaSuccess) trace = nullptr;
@@ -71,7 +60,6 @@ Ctx::~Ctx() {
   }
   for (auto e : free_events_) cudaEventDestroy(e);
   if (cur_start_) cudaEventDestroy(cur_start_);
-  if (counters_) cudaFree(counters_);
   if (identity_) cudaFree(identity_);
   if (trace) cudaFree(trace);
   if (ltrace_) cudaFree(ltrace_);

@@ -55,12 +55,6 @@ struct GemmReq {
   bool a_stream_once;  // A operand is read once (evict-first hint)
   int cg;              // 1: one CTA per 128-row tile; 2: CTA pair (cta_group::2) per 256-row tile
   KernelId kid;
-  // in-kernel deterministic split-K fix-up (OUT_F32 + splits): see Prob in tc_gemm.cuh
-  int* counters;
-  int fix_cols;
-  void* fix_out;
-  int64_t fix_ldo;
-  int fix_bf16, fix_transpose, fix_accumulate;
   int fold, fold_w;  // OUT_F32_FOLD
   bool tail_diag;  // a2 = 128x128 identity, b2 read at the tile's own rows (see Prob)
   int a_policy;      // L2 policy of the A operand: 0 from a_stream_once, 1 normal, 2 evict-first
@@ -86,10 +80,6 @@ class Ctx {
   int device() const { return device_; }
   int num_sms() const { return num_sms_; }
   int main_cg() const { return main_cg_; }  // CTA-group size of the Y / dX GEMMs (env RUNLORA_MAIN_CG)
-  // Split-K tile counters (device, zero between launches; owned by the handle).
-  static constexpr int kCounterCap = 1 << 16;
-  int* counters() const { return counters_; }
-  bool fixup_enabled() const { return counters_ != nullptr && fixup_; }
   bool occ2() const { return occ2_; }  // 2 CTAs/SM for rank-r kernels (env RUNLORA_OCC2=0 disables)
   bool pdl() const { return pdl_; }    // programmatic dependent launch (env RUNLORA_PDL=0 disables)
   // split-K reductions of a backward whose launch waits until after its dX GEMM (same stream)
@@ -134,11 +124,9 @@ class Ctx {
   int device_;
   int num_sms_ = 148;
   int main_cg_ = 2;
-  int* counters_ = nullptr;
   void* identity_ = nullptr;
   bool tma_store_main_ = false;   // env RUNLORA_TMA_STORE_MAIN=1
   bool tma_store_wprime_ = true;  // env RUNLORA_TMA_STORE_WPRIME=0
-  bool fixup_ = false;     // env RUNLORA_SPLITK_FIXUP=1: in-kernel fix-up instead of the reducer launch
   bool occ2_ = true;
   bool pdl_ = true;
   CUtensorMapL2promotion promo_mn_ = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;  // 3-D (MN-major) boxes       // env RUNLORA_OCC2=0: one CTA per SM for the rank-r kernels too

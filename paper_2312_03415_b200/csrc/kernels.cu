@@ -329,13 +329,6 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
     p.split_stride = r.split_stride;
     p.Cin = static_cast<const __nv_bfloat16*>(r.Cin);
     p.ldc = r.ldc;
-    p.counters = r.counters;
-    p.fix_cols = r.fix_cols;
-    p.fix_out = r.fix_out;
-    p.fix_ldo = r.fix_ldo;
-    p.fix_bf16 = r.fix_bf16;
-    p.fix_transpose = r.fix_transpose;
-    p.fix_accumulate = r.fix_accumulate;
     p.fold = r.fold;
     p.fold_w = r.fold_w;
     if (r.out_mode == OUT_F32_FOLD &&

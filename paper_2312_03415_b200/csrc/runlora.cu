@@ -223,12 +223,6 @@ runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, KernelI
   const SkinnyPlan p = plan_skinny(jobs, n);
   GemmReq q[2];
   ReduceJob rj[2];
-  // in-kernel fix-up needs one counter per output tile of each job
-  int64_t tiles_total = 0;
-  for (int i = 0; i < n; ++i)
-    tiles_total += ((jobs[i].rows + kBM - 1) / kBM) * (p.Npad[i] / p.BN[i]);
-  const bool fixup = !p.direct && c.fixup_enabled() && tiles_total <= Ctx::kCounterCap;
-  int64_t ctr_off = 0;
   for (int i = 0; i < n; ++i) {
     const Skinny& j = jobs[i];
     q[i] = base_req((int)j.rows, p.direct ? (int)j.r : p.Npad[i], kid);
@@ -251,16 +245,6 @@ runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, KernelI
       q[i].split_stride = j.rows * (int64_t)p.Npad[i];
       q[i].splits = p.splits[i];
       q[i].kb_per_split = p.kps[i];
-      if (fixup) {
-        q[i].counters = c.counters() + ctr_off;
-        ctr_off += ((j.rows + kBM - 1) / kBM) * (p.Npad[i] / p.BN[i]);
-        q[i].fix_cols = (int)j.r;
-        q[i].fix_out = j.out;
-        q[i].fix_ldo = j.ldo;
-        q[i].fix_bf16 = j.out_bf16 ? 1 : 0;
-        q[i].fix_transpose = j.transpose ? 1 : 0;
-        q[i].fix_accumulate = j.accumulate ? 1 : 0;
-      }
     }
     rj[i] = ReduceJob{Pi, p.splits[i], j.rows * (int64_t)p.Npad[i], (int)j.rows, (int)j.r, p.Npad[i], j.out,
                       j.out_bf16 ? 1 : 0, j.ldo, j.transpose ? 1 : 0, j.accumulate ? 1 : 0};
@@ -268,7 +252,7 @@ runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, KernelI
   std::string err;
   cudaError_t e = launch_tc_gemm(c, q, n, st, &err);
   if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
-  if (!p.direct && !fixup) {
+  if (!p.direct) {
     if (defer_reduce) {
       c.deferred_reduce.assign(rj, rj + n);
       return RUNLORA_OK;
@@ -969,10 +953,10 @@ runlora_status_t runlora_create(runlora_handle_t* out, int device) {
   try {
     runlora_handle_s* h = new runlora_handle_s;
     h->ctx = new Ctx(device);
-    if (!h->ctx->identity() || !h->ctx->counters()) {
+    if (!h->ctx->identity()) {
       delete h->ctx;
       delete h;
-      return fail(RUNLORA_ERR_CUDA, "device allocation of the handle's identity tile / counters failed");
+      return fail(RUNLORA_ERR_CUDA, "device allocation of the handle's identity tile failed");
     }
     *out = h;
   } catch (...) {

@@ -64,14 +64,6 @@ struct Prob {
   const __nv_bfloat16* Cin;  // OUT_BF16_ADD: added matrix [M, ldc]
   long long ldc;
   uint64_t hint_a, hint_b;   // TMA L2 cache hints
-  // Split-K fix-up (OUT_F32 with counters != nullptr): the LAST unit of an output tile to
-  // finish sums the fp32 slabs of all splits in fixed split order (deterministic) and
-  // writes the final out (fp32/bf16, optionally transposed/accumulated); counters self-reset.
-  int* counters;
-  int fix_cols;              // valid output columns (r)
-  void* fix_out;
-  long long fix_ldo;
-  int fix_bf16, fix_transpose, fix_accumulate;
   int fold, fold_w;  // OUT_F32_FOLD
   // Block-diagonal concat-K tail: the tail A operand is the 128x128 identity (A2, loaded at
   // M coordinate 0) and the tail B operand is read at K coordinate m0 + k, i.e. the rows of
@@ -206,76 +198,6 @@ __device__ __forceinline__ void store_row_segment(const Prob& p, int split, int 
   }
 }
 
-// Epilogue warps (4..7, 128 threads) only: named barrier 1.
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-
-// Deterministic split-K fix-up, run by the 128 epilogue threads after their unit's fp32
-// slab is stored: the last-arriving unit of the tile reduces all slabs in split order.
-__device__ __forceinline__ bool splitk_fixup(const Prob& p, const Unit& t, int m0, int n0, int row, int* s_flag) {
-  __threadfence();
-  epi_bar();
-  const int tile = t.m_blk * p.num_n_tiles + t.n_blk;
-  if (threadIdx.x == 4 * 32) {
-    const int old = atomicAdd(&p.counters[tile], 1);
-    *s_flag = (old == p.num_splits - 1) ? 1 : 0;
-  }
-  epi_bar();
-  const int last = *s_flag;
-  epi_bar();  // everyone has read the flag before it can be rewritten for the next unit
-  if (!last) return false;
-  __threadfence();
-  if (row < p.M) {
-    // up to 4 splits x 4 column groups (16 loads) in flight, summed in split order
-    const int c_end = min(n0 + p.bn, p.fix_cols);
-    const float* src = static_cast<const float*>(p.D) + (long long)row * p.ldd;
-    for (int c = n0; c < c_end; c += 16) {
-      float4 acc[4];
-#pragma unroll
-      for (int gi = 0; gi < 4; ++gi) acc[gi] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int s0 = 0; s0 < p.num_splits; s0 += 4) {
-        float4 v[4][4];
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-          for (int gi = 0; gi < 4; ++gi)
-            if (s0 + x < p.num_splits && c + 4 * gi < c_end)
-              v[x][gi] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + x) * p.split_stride + c + 4 * gi));
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-          for (int gi = 0; gi < 4; ++gi)
-            if (s0 + x < p.num_splits && c + 4 * gi < c_end) {
-              acc[gi].x += v[x][gi].x;
-              acc[gi].y += v[x][gi].y;
-              acc[gi].z += v[x][gi].z;
-              acc[gi].w += v[x][gi].w;
-            }
-      }
-#pragma unroll
-      for (int gi = 0; gi < 4; ++gi) {
-        const float a4[4] = {acc[gi].x, acc[gi].y, acc[gi].z, acc[gi].w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int col = c + 4 * gi + e;
-          if (col >= c_end) break;
-          const long long o = p.fix_transpose ? (long long)col * p.fix_ldo + row : (long long)row * p.fix_ldo + col;
-          float v = a4[e];
-          if (p.fix_bf16) {
-            __nv_bfloat16* d = static_cast<__nv_bfloat16*>(p.fix_out) + o;
-            if (p.fix_accumulate) v += __bfloat162float(*d);
-            *d = __float2bfloat16_rn(v);
-          } else {
-            float* d = static_cast<float*>(p.fix_out) + o;
-            if (p.fix_accumulate) v += *d;
-            *d = v;
-          }
-        }
-      }
-    }
-  }
-  if (threadIdx.x == 4 * 32) p.counters[tile] = 0;  // ready for the next launch
-  return true;
-}
 
 // EPI = 0: epilogue stores from registers; EPI = 3: TMA-store epilogue (plain bf16 outputs).
 template <int BN_MAX, int CG, int OCC = 1, int EPI = 0>
@@ -294,7 +216,6 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  __shared__ int s_flag[1];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -572,7 +493,6 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote<CG>(&tempty[acc], 0);  // leader's barrier
-      if (p.counters) splitk_fixup(p, t, m0, n0, row, s_flag);
       if (g.trace && threadIdx.x == 4 * 32) g.trace[8 * u + 3] = globaltimer();
     }
     if constexpr (EPI == 3) {
