@@ -131,3 +131,66 @@ def test_fp32_c1_selected_pair_through_autograd(rl):
     wA, wB, wX = O.reference_backward(Xn, Wn, An, Bn, dYn)
     for g, w in ((A.grad, wA), (B.grad, wB), (X.grad, wX)):
         assert O.rel_fro(_np(g), w) <= 1e-5
+
+
+@pytest.mark.parametrize("plan", [(1, 1), (2, 5)])
+def test_cuda_graph_capture_bit_exact(rl, plan):
+    """A forward+backward captured in a CUDA graph (every launch on the caller's stream, no
+    host synchronisation inside the calls, PDL edges kept) replays bit-exactly and matches
+    the oracle."""
+    c = synth.case("graph", 0, 24, 640, 1024, 768, 16, "bf16")
+    ops, d, shape, out = _setup(rl, c)
+    h = rl.handle(0)
+    ws = h.workspace(shape)
+    f, b = plan
+
+    def step():
+        h.forward(f, shape, d["X"], d["W"], d["A"], d["B"], out["Y"], ws)
+        h.backward(b, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], out["dX"], out["dA"], out["dB"], ws=ws)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    ref = {k: v.clone() for k, v in out.items()}
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for v in out.values():
+        v.fill_(float("nan"))
+    g.replay()
+    torch.cuda.synchronize()
+    for k, v in out.items():
+        assert torch.equal(v, ref[k]), k
+    Xn, Wn, An, Bn, dYn = (_np(ops[k]) for k in ("X", "W", "A", "B", "dY"))
+    wA, wB, wX = O.reference_backward(Xn, Wn, An, Bn, dYn)
+    assert O.rel_fro(_np(out["Y"]), O.forward(1, Xn, Wn, An, Bn)) <= TOL
+    for k, w in (("dA", wA), ("dB", wB), ("dX", wX)):
+        assert O.rel_fro(_np(out[k]), w) <= TOL, k
+
+
+def test_launch_timeline_records(rl, monkeypatch):
+    """Launch records (RUNLORA_LTRACE, read at handle creation): one per library launch,
+    entry <= ready <= exit, in launch order on one stream."""
+    import ctypes as C
+    monkeypatch.setenv("RUNLORA_LTRACE", "1")
+    c = synth.case("ltrace", 0, 25, 1024, 1024, 1024, 16, "bf16")
+    ops, d, shape, out = _setup(rl, c)
+    h = rl.Handle(0)  # fresh handle: reads the environment
+    lib = rl._lib
+    lib.runlora_debug_ltrace.restype = C.c_int
+    buf = np.zeros(8 * 4096, dtype=np.uint64)
+    kids = np.zeros(4096, dtype=np.int32)
+    args = (h._h, buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), kids.ctypes.data_as(C.POINTER(C.c_int)), 4096)
+    lib.runlora_debug_ltrace(*args)
+    l0 = h.launch_count()
+    h.forward(2, shape, d["X"], d["W"], d["A"], d["B"], out["Y"])
+    h.backward(1, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], out["dX"], out["dA"], out["dB"])
+    n = lib.runlora_debug_ltrace(*args)
+    assert n == h.launch_count() - l0 > 0
+    rec = buf[: 8 * n].reshape(n, 8).astype(np.int64)
+    assert np.all(rec[:, 0] <= rec[:, 1]) and np.all(rec[:, 1] <= rec[:, 2]) and np.all(rec[:, 2] <= rec[:, 4])
+    assert np.all(rec[:, 3] <= rec[:, 4])
+    assert np.all(np.diff(rec[:, 1]) > 0)  # PDL: each launch becomes ready after its predecessor
