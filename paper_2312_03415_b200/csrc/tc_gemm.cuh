@@ -97,10 +97,13 @@ constexpr int kGemmThreads = 256;
 
 // OCC = CTAs per SM (2 for the HBM-bound rank-r kernels: twice the TMA requests in flight).
 // EPI = 3: TMA-store epilogue (bf16 tile staged per warp in swizzled smem).
-template <int BN_MAX, int CG, int OCC = 1, int EPI = 0>
+// KS = 64-wide K atoms per pipeline stage (1 or 2): a stage holds KS A atoms then KS B atoms.
+template <int BN_MAX, int CG, int OCC = 1, int EPI = 0, int KS = 1>
 struct TileCfg {
-  static constexpr uint32_t A_BYTES = kBM * kBK * 2;
-  static constexpr uint32_t B_BYTES = (BN_MAX / CG) * kBK * 2;
+  static constexpr uint32_t A_ATOM = kBM * kBK * 2;
+  static constexpr uint32_t B_ATOM = (BN_MAX / CG) * kBK * 2;
+  static constexpr uint32_t A_BYTES = KS * A_ATOM;
+  static constexpr uint32_t B_BYTES = KS * B_ATOM;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   // EPI = 3: per epilogue warp kStgBufs 32-row x 64-column bf16 staging tiles (128B swizzle)
   static constexpr uint32_t STG_BYTES = EPI == 3 ? 4 * kStgBufs * 4096 : 0;
@@ -200,10 +203,11 @@ __device__ __forceinline__ void store_row_segment(const Prob& p, int split, int 
 
 
 // EPI = 0: epilogue stores from registers; EPI = 3: TMA-store epilogue (plain bf16 outputs).
-template <int BN_MAX, int CG, int OCC = 1, int EPI = 0>
+// KS: 64-wide K atoms per pipeline stage (TileCfg).
+template <int BN_MAX, int CG, int OCC = 1, int EPI = 0, int KS = 1>
 __global__ void __launch_bounds__(kGemmThreads, OCC)
     tc_gemm_kernel(const __grid_constant__ Tmaps tm, const __grid_constant__ GemmArgs g) {
-  using C = TileCfg<BN_MAX, CG, OCC, EPI>;
+  using C = TileCfg<BN_MAX, CG, OCC, EPI, KS>;
   constexpr int STAGES = C::STAGES;
   static_assert(BN_MAX % (16 * CG) == 0 && BN_MAX >= 16 && BN_MAX <= 256, "UMMA N");
 
@@ -283,35 +287,39 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       if (g.dbg == 1 || g.dbg >= 3) continue;
       const int cw = p.b_swz >> 1;   // MN-major B chunk width (elements)
       const int cb = p.b_swz * kBK;  // MN-major B chunk bytes (64 K-rows)
-      for (int i = 0; i < nkb; ++i) {
+      for (int i0 = 0; i0 < nkb; i0 += KS) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (elect_one_sync()) {
-          uint8_t* a = sA + stage * C::A_BYTES;
-          uint8_t* b = sB + stage * C::B_BYTES;
+          const int natoms = min(KS, nkb - i0);
           uint64_t* fb = &full[stage];
-          if (leader) mbar_arrive_expect_tx(fb, p.stage_tx);
-          const bool tail = i >= nmain;
-          const bool diag = tail && p.tail_diag;
-          const CUtensorMap* ta = &tm.m[t.prob][tail ? 2 : 0];
-          const CUtensorMap* tb = &tm.m[t.prob][tail ? 3 : 1];
-          const int ki = rev ? nmain - 1 - i : i;
-          const int kc = (tail ? (i - nmain) : (kb0 + ki)) * kBK;
-          const int ma = diag ? 0 : m0;          // identity tail: rows of I
-          const int kcb = diag ? m0 + kc : kc;   // identity tail: B2 rows of this tile
-          if (!p.a_mn) {
-            tma_load_2d<CG>(ta, fb, a, kc, ma, p.hint_a);
-          } else if (p.a_3d) {
-            tma_load_3d<CG>(ta, fb, a, 0, kc, ma >> 6, p.hint_a);
-          } else {
-            tma_load_2d<CG>(ta, fb, a, ma, kc, p.hint_a);
-            tma_load_2d<CG>(ta, fb, a + 8192, ma + 64, kc, p.hint_a);
-          }
-          if (!p.b_mn) {
-            tma_load_2d<CG>(tb, fb, b, kcb, n0, p.hint_b);
-          } else if (p.b_3d) {
-            tma_load_3d<CG>(tb, fb, b, 0, kcb, n0 / cw, p.hint_b);
-          } else {
-            for (int h = 0; h < nb / cw; ++h) tma_load_2d<CG>(tb, fb, b + h * cb, n0 + cw * h, kcb, p.hint_b);
+          if (leader) mbar_arrive_expect_tx(fb, p.stage_tx * (uint32_t)natoms);
+          for (int at = 0; at < natoms; ++at) {
+            const int i = i0 + at;
+            uint8_t* a = sA + stage * C::A_BYTES + at * C::A_ATOM;
+            uint8_t* b = sB + stage * C::B_BYTES + at * C::B_ATOM;
+            const bool tail = i >= nmain;
+            const bool diag = tail && p.tail_diag;
+            const CUtensorMap* ta = &tm.m[t.prob][tail ? 2 : 0];
+            const CUtensorMap* tb = &tm.m[t.prob][tail ? 3 : 1];
+            const int ki = rev ? nmain - 1 - i : i;
+            const int kc = (tail ? (i - nmain) : (kb0 + ki)) * kBK;
+            const int ma = diag ? 0 : m0;          // identity tail: rows of I
+            const int kcb = diag ? m0 + kc : kc;   // identity tail: B2 rows of this tile
+            if (!p.a_mn) {
+              tma_load_2d<CG>(ta, fb, a, kc, ma, p.hint_a);
+            } else if (p.a_3d) {
+              tma_load_3d<CG>(ta, fb, a, 0, kc, ma >> 6, p.hint_a);
+            } else {
+              tma_load_2d<CG>(ta, fb, a, ma, kc, p.hint_a);
+              tma_load_2d<CG>(ta, fb, a + 8192, ma + 64, kc, p.hint_a);
+            }
+            if (!p.b_mn) {
+              tma_load_2d<CG>(tb, fb, b, kcb, n0, p.hint_b);
+            } else if (p.b_3d) {
+              tma_load_3d<CG>(tb, fb, b, 0, kcb, n0 / cw, p.hint_b);
+            } else {
+              for (int h = 0; h < nb / cw; ++h) tma_load_2d<CG>(tb, fb, b + h * cb, n0 + cw * h, kcb, p.hint_b);
+            }
           }
         }
         __syncwarp();
@@ -350,19 +358,23 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       const uint32_t b_step = p.b_mn ? 16u * b_swz : 32u;
       const uint64_t a_hi = smem_desc(0, p.a_mn ? 8192 : 16, 1024, 2u);
       const uint64_t b_hi = smem_desc(0, p.b_mn ? 64u * b_swz : 16u, 8u * b_swz, sw_layout_code(b_swz));
-      for (int i = 0; i < nkb; ++i) {
+      for (int i0 = 0; i0 < nkb; i0 += KS) {
         if (g.dbg != 1 && g.dbg < 3) mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const int ki = rev ? nmain - 1 - i : i;
-        const int kleft = (i < nmain) ? (p.k1 - (kb0 + ki) * kBK) : (p.k2 - (i - nmain) * kBK);
-        const int ksteps = min(kBK / 16, (kleft + 15) >> 4);
-        const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
-        const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+        const int natoms = min(KS, nkb - i0);
         if (elect_one_sync()) {
-          for (int j = 0; j < (g.dbg == 2 ? 0 : ksteps); ++j) {
-            const uint64_t ad = a_hi | (uint64_t)(((a_addr + j * a_step) >> 4) & 0x3FFF);
-            const uint64_t bd = b_hi | (uint64_t)(((b_addr + j * b_step) >> 4) & 0x3FFF);
-            umma_f16<CG>(d_tmem, ad, bd, p.idesc, (i > 0 || j > 0) ? 1u : 0u);
+          for (int at = 0; at < natoms; ++at) {
+            const int i = i0 + at;
+            const int ki = rev ? nmain - 1 - i : i;
+            const int kleft = (i < nmain) ? (p.k1 - (kb0 + ki) * kBK) : (p.k2 - (i - nmain) * kBK);
+            const int ksteps = min(kBK / 16, (kleft + 15) >> 4);
+            const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES + at * C::A_ATOM);
+            const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES + at * C::B_ATOM);
+            for (int j = 0; j < (g.dbg == 2 ? 0 : ksteps); ++j) {
+              const uint64_t ad = a_hi | (uint64_t)(((a_addr + j * a_step) >> 4) & 0x3FFF);
+              const uint64_t bd = b_hi | (uint64_t)(((b_addr + j * b_step) >> 4) & 0x3FFF);
+              umma_f16<CG>(d_tmem, ad, bd, p.idesc, (i > 0 || j > 0) ? 1u : 0u);
+            }
           }
           umma_commit<CG>(&empty[stage]);  // frees the smem slot(s) when these MMAs retire
         }
