@@ -57,7 +57,10 @@ RMS_EPS = 1e-6
 
 
 def rms(z: torch.Tensor) -> torch.Tensor:
-    """Row-wise z / sqrt(mean(z²) + eps), computed in fp32, returned in z's dtype."""
+    """Row-wise z / sqrt(mean(z²) + eps) (weightless), fp32 statistics, z's dtype out —
+    torch's fused rms_norm (one pass forward and backward) when available."""
+    if hasattr(torch.nn.functional, "rms_norm"):
+        return torch.nn.functional.rms_norm(z, (z.shape[-1],), None, RMS_EPS)
     zf = z.float()
     return (zf * torch.rsqrt(zf.pow(2).mean(dim=-1, keepdim=True) + RMS_EPS)).to(z.dtype)
 
