@@ -198,6 +198,30 @@ typedef struct {
 runlora_status_t runlora_step_host(runlora_handle_t h, const runlora_shape_t* s, const runlora_host_step_t* st,
                                    void* workspace, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------- quantized frozen weight (QLoRA-style)
+ * "functionality to work with quantized model weights to fine-tune models in fashion of
+ * QLoRA" (no format given).  Format (R18): FP8 E4M3 (OCP E4M3FN: bias 7,
+ * max 448, no infinities) with one fp32 scale per output column:
+ *   scale[j] = max_i |W[i, j]| / 448 (1 for an all-zero column),
+ *   Wq[i, j] = e4m3_rn_satfinite(W[i, j] / scale[j])      (Wq: k x m bytes, row-major)
+ *   W~[i, j] = bf16_rn(fp32(e4m3(Wq[i, j])) * scale[j])   (what the hot path multiplies by).
+ * runlora_quantize_w_e4m3: W bf16 [k, m] (device) -> Wq, scale (device; scale 16-byte
+ *   aligned, m a multiple of 8).  Asynchronous on `stream`.
+ * runlora_forward_wq / runlora_backward_wq: as runlora_forward / runlora_backward with W
+ *   given as (Wq, scale); every call dequantizes W~ into the workspace (after the regular
+ *   workspace) and runs the unchanged variants on it, so only Wq + scale persist between
+ *   calls (half of the bf16 W).  Workspace: runlora_workspace_size_wq bytes. */
+runlora_status_t runlora_quantize_w_e4m3(runlora_handle_t h, int64_t k, int64_t m, const void* W, void* Wq,
+                                         float* scale, void* stream);
+runlora_status_t runlora_workspace_size_wq(const runlora_shape_t* s, int fwd, int bwd, size_t* bytes);
+runlora_status_t runlora_forward_wq(runlora_handle_t h, int fwd, const runlora_shape_t* s, const void* X,
+                                    const void* Wq, const float* scale, const void* A, const void* B, void* Y,
+                                    void* workspace, size_t ws_bytes, void* stream);
+runlora_status_t runlora_backward_wq(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X,
+                                     const void* Wq, const float* scale, const void* A, const void* B,
+                                     const void* dY, void* dX, void* dA, void* dB, int grad_dtype, int accumulate,
+                                     void* workspace, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- tracing
  * When enabled, every kernel the library launches is bracketed by CUDA events
  * on its stream; runlora_profile_read synchronises those events and returns

@@ -25,6 +25,8 @@ enum KernelId : int {
   KID_SPLITK_REDUCE,   // fixed-order split-K reduction / cast / transpose
   KID_SGEMM_F32,       // fp32 SIMT GEMM (RUNLORA_F32 path)
   KID_REPEAT_COLS,     // A repeated along its columns (dX tail against Z1's partial blocks)
+  KID_QUANT,           // W -> FP8 E4M3 + per-column scales (column max, quantize, finalize)
+  KID_DEQUANT,         // FP8 E4M3 W -> bf16 W in the workspace (QLoRA-style entry points)
   KID_COUNT
 };
 extern const char* const kKernelNames[KID_COUNT];
@@ -171,6 +173,11 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
 // out (fp32 or bf16; optionally transposed: out[j*ldo + i]; optionally accumulated).
 
 cudaError_t launch_splitk_reduce(Ctx& ctx, const ReduceJob* jobs, int njobs, cudaStream_t s);
+// Quantized frozen weight (quant.cu): W[k, m] bf16 -> Wq e4m3 bytes + scale[m] fp32, and back
+// to bf16 (m multiple of 8, scale 16-byte aligned).
+cudaError_t launch_quantize_w(Ctx& ctx, const void* W, int64_t k, int64_t m, void* Wq, float* scale, cudaStream_t s);
+cudaError_t launch_dequantize_w(Ctx& ctx, const void* Wq, const float* scale, int64_t k, int64_t m, void* W,
+                                cudaStream_t s);
 // dst[i, t*cols + j] = src[i, j] for t < reps (bf16, row-major; 16-byte column groups).
 cudaError_t launch_repeat_cols(Ctx& ctx, const void* src, int rows, int cols, int reps, void* dst, cudaStream_t s);
 // fp32 SIMT GEMM: C[i,j] = (acc ? C[i,j] : 0) + (Cadd ? Cadd[i,j] : 0) + sum_t A(i,t) B(t,j),

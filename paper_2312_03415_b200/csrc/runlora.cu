@@ -1133,6 +1133,75 @@ runlora_status_t runlora_backward_input(runlora_handle_t h, int bwd, const runlo
   return do_input(h, bwd, s, W, A, B, dY, dX, ws, ws_bytes, stream);
 }
 
+// ------------------------------------------------ quantized frozen weight (R18)
+runlora_status_t runlora_quantize_w_e4m3(runlora_handle_t h, int64_t k, int64_t m, const void* W, void* Wq,
+                                         float* scale, void* stream) {
+  RL_TRY(check_handle(h));
+  if (k <= 0 || m <= 0) return fail(RUNLORA_ERR_INVALID_ARG, "k and m must be >= 1");
+  if (m & 7) return fail(RUNLORA_ERR_ALIGNMENT, "m must be a multiple of 8");
+  RL_TRY(check_ptr(W, "W"));
+  RL_TRY(check_ptr(Wq, "Wq"));
+  RL_TRY(check_ptr(scale, "scale"));
+  DeviceGuard dg(h->ctx->device());
+  cudaError_t e = launch_quantize_w(*h->ctx, W, k, m, Wq, scale, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "quantize launch");
+  return RUNLORA_OK;
+}
+
+runlora_status_t runlora_workspace_size_wq(const runlora_shape_t* s, int fwd, int bwd, size_t* bytes) {
+  RL_TRY(runlora_workspace_size(s, fwd, bwd, bytes));
+  if (s->dtype != RUNLORA_BF16) return fail(RUNLORA_ERR_DTYPE, "quantized W needs bf16 operands");
+  *bytes += al((size_t)s->k * s->m * 2);  // the dequantized W, after the regular workspace
+  return RUNLORA_OK;
+}
+
+namespace {
+// Dequantizes Wq into the tail of the workspace; returns the bf16 W and the regular
+// workspace size that precedes it.
+runlora_status_t dequant_into_ws(runlora_handle_t h, const runlora_shape_t* s, const void* Wq, const float* scale,
+                                 void* ws, size_t ws_bytes, void* stream, const void** W, size_t* ws_main) {
+  RL_TRY(check_handle(h));
+  RL_TRY(check_shape(s));
+  if (s->dtype != RUNLORA_BF16) return fail(RUNLORA_ERR_DTYPE, "quantized W needs bf16 operands");
+  RL_TRY(check_ptr(Wq, "Wq"));
+  RL_TRY(check_ptr(scale, "scale"));
+  if (!ws) return fail(RUNLORA_ERR_INVALID_ARG, "workspace is NULL");
+  const size_t main = layout_of(*s).total;
+  if (ws_bytes < main + al((size_t)s->k * s->m * 2)) {
+    char b[160];
+    snprintf(b, sizeof b, "workspace too small for the quantized-W entry points: %zu bytes given, %zu needed",
+             ws_bytes, main + al((size_t)s->k * s->m * 2));
+    return fail(RUNLORA_ERR_WORKSPACE, b);
+  }
+  void* wdq = static_cast<char*>(ws) + main;
+  DeviceGuard dg(h->ctx->device());
+  cudaError_t e = launch_dequantize_w(*h->ctx, Wq, scale, s->k, s->m, wdq, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "dequantize launch");
+  *W = wdq;
+  *ws_main = main;
+  return RUNLORA_OK;
+}
+}  // namespace
+
+runlora_status_t runlora_forward_wq(runlora_handle_t h, int fwd, const runlora_shape_t* s, const void* X,
+                                    const void* Wq, const float* scale, const void* A, const void* B, void* Y,
+                                    void* ws, size_t ws_bytes, void* stream) {
+  const void* W = nullptr;
+  size_t main = 0;
+  RL_TRY(dequant_into_ws(h, s, Wq, scale, ws, ws_bytes, stream, &W, &main));
+  return do_forward(h, fwd, s, X, W, A, B, Y, ws, main, stream);
+}
+
+runlora_status_t runlora_backward_wq(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X,
+                                     const void* Wq, const float* scale, const void* A, const void* B,
+                                     const void* dY, void* dX, void* dA, void* dB, int grad_dtype, int accumulate,
+                                     void* ws, size_t ws_bytes, void* stream) {
+  const void* W = nullptr;
+  size_t main = 0;
+  RL_TRY(dequant_into_ws(h, s, Wq, scale, ws, ws_bytes, stream, &W, &main));
+  return do_backward(h, bwd, s, X, W, A, B, dY, dX, dA, dB, grad_dtype, accumulate, ws, main, stream);
+}
+
 runlora_status_t runlora_step_host(runlora_handle_t h, const runlora_shape_t* s, const runlora_host_step_t* t,
                                    void* ws, size_t ws_bytes, void* stream) {
   RL_TRY(check_handle(h));

@@ -20,6 +20,10 @@ def _shape(X, W, A):
     return rl.make_shape(n, k, m, r, X.dtype)
 
 
+def _is_q(W):
+    return isinstance(W, rl.QuantizedWeight)
+
+
 class GradSink:
     """fp32 destination of one linear's adapter gradients (views dA [k, r], dB [r, m], e.g.
     into a data-parallel bucket): the backward accumulates into them (micro-batching,
@@ -41,14 +45,21 @@ class LoRALinearFunction(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, X, W, A, B, fwd: int, bwd: int, sink: GradSink | None = None):
-        for t, name in ((X, "X"), (W, "W"), (A, "A"), (B, "B")):
+        # W: a frozen bf16/fp32 tensor, or an rl.QuantizedWeight (FP8 E4M3 + column scales)
+        for t, name in ((X, "X"), (W.q if _is_q(W) else W, "W"), (A, "A"), (B, "B")):
             if not t.is_cuda or not t.is_contiguous():
                 raise ValueError(f"{name} must be a contiguous CUDA tensor")
         shape = _shape(X, W, A)
         h = rl.handle(X.device)
         Y = torch.empty(X.shape[0], W.shape[1], dtype=X.dtype, device=X.device)
-        h.forward(fwd, shape, X, W, A, B, Y)
-        ctx.save_for_backward(X, W, A, B)   # no XA
+        if _is_q(W):
+            h.forward_wq(fwd, shape, X, W, A, B, Y)
+            ctx.wq = W
+            ctx.save_for_backward(X, A, B)  # no XA; W stays quantized
+        else:
+            h.forward(fwd, shape, X, W, A, B, Y)
+            ctx.wq = None
+            ctx.save_for_backward(X, W, A, B)   # no XA
         ctx.bwd = bwd
         ctx.sink = sink
         ctx.need_dx = ctx.needs_input_grad[0]
@@ -56,20 +67,25 @@ class LoRALinearFunction(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, dY):
-        X, W, A, B = ctx.saved_tensors
+        if ctx.wq is not None:
+            X, A, B = ctx.saved_tensors
+            W = ctx.wq
+            run = rl.handle(X.device).backward_wq
+        else:
+            X, W, A, B = ctx.saved_tensors
+            run = rl.handle(X.device).backward
         dY = dY.contiguous()
         shape = _shape(X, W, A)
-        h = rl.handle(X.device)
         dX = torch.empty_like(X) if ctx.need_dx else None
         sink = ctx.sink
         if sink is not None:
-            h.backward(ctx.bwd, shape, X, W, A, B, dY, dX, sink.dA, sink.dB, accumulate=sink.accumulate)
+            run(ctx.bwd, shape, X, W, A, B, dY, dX, sink.dA, sink.dB, accumulate=sink.accumulate)
             sink.ready()
             return dX, None, None, None, None, None, None
         gdt = torch.float32 if X.dtype == torch.float32 else A.dtype
         dA = torch.empty(A.shape, dtype=gdt, device=X.device)
         dB = torch.empty(B.shape, dtype=gdt, device=X.device)
-        h.backward(ctx.bwd, shape, X, W, A, B, dY, dX, dA, dB)
+        run(ctx.bwd, shape, X, W, A, B, dY, dX, dA, dB)
         return dX, None, dA.to(A.dtype), dB.to(B.dtype), None, None, None
 
 

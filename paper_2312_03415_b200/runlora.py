@@ -70,7 +70,8 @@ class KernelStat(C.Structure):
 EXPORTS = ["runlora_version", "runlora_create", "runlora_destroy", "runlora_flops", "runlora_param_reduction",
            "runlora_workspace_size", "runlora_select", "runlora_forward", "runlora_backward",
            "runlora_backward_params", "runlora_backward_input", "runlora_step_host", "runlora_profile_enable",
-           "runlora_profile_read", "runlora_launch_count", "runlora_status_string", "runlora_last_error"]
+           "runlora_profile_read", "runlora_launch_count", "runlora_status_string", "runlora_last_error",
+           "runlora_quantize_w_e4m3", "runlora_workspace_size_wq", "runlora_forward_wq", "runlora_backward_wq"]
 
 
 def _load():
@@ -98,6 +99,10 @@ def _load():
         "runlora_launch_count": (U64, [P]),
         "runlora_status_string": (C.c_char_p, [I]),
         "runlora_last_error": (C.c_char_p, []),
+        "runlora_quantize_w_e4m3": (I, [P, C.c_int64, C.c_int64, P, P, P, P]),
+        "runlora_workspace_size_wq": (I, [S, I, I, C.POINTER(SZ)]),
+        "runlora_forward_wq": (I, [P, I, S, P, P, P, P, P, P, P, SZ, P]),
+        "runlora_backward_wq": (I, [P, I, S, P, P, P, P, P, P, P, P, P, I, I, P, SZ, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -147,6 +152,28 @@ def workspace_size(shape: Shape, fwd: int = 0, bwd: int = 0) -> int:
     return int(out.value)
 
 
+class QuantizedWeight:
+    """A frozen W [k, m] stored as FP8 E4M3 bytes `q` with one fp32 `scale` per output
+    column (R18); `shape` is (k, m)."""
+
+    def __init__(self, q: torch.Tensor, scale: torch.Tensor):
+        self.q, self.scale = q, scale
+
+    @property
+    def shape(self):
+        return tuple(self.q.shape)
+
+    @property
+    def device(self):
+        return self.q.device
+
+
+def workspace_size_wq(shape: Shape) -> int:
+    out = C.c_size_t()
+    _check(_lib.runlora_workspace_size_wq(C.byref(shape), 0, 0, C.byref(out)), "runlora_workspace_size_wq")
+    return out.value
+
+
 def select_by_flops(shape: Shape) -> Plan:
     p = Plan()
     _check(_lib.runlora_select(None, C.byref(shape), BY_FLOPS, None, None, 0, None, C.byref(p)), "runlora_select")
@@ -186,11 +213,34 @@ class Handle:
             pass
 
     # workspace: plain device memory owned by the caller side of the ABI
-    def workspace(self, shape: Shape) -> torch.Tensor:
-        need = workspace_size(shape)
+    def workspace(self, shape: Shape, quantized_w: bool = False) -> torch.Tensor:
+        need = workspace_size_wq(shape) if quantized_w else workspace_size(shape)
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
         return self._ws
+
+    # ------------------------------------------------- quantized frozen W (R18)
+    def quantize_w(self, W: torch.Tensor):
+        """W bf16 [k, m] -> QuantizedWeight (FP8 E4M3 bytes [k, m], fp32 scale [m])."""
+        k, m = W.shape
+        Wq = torch.empty(k, m, dtype=torch.uint8, device=W.device)
+        scale = torch.empty(m, dtype=torch.float32, device=W.device)
+        _check(_lib.runlora_quantize_w_e4m3(self._h, k, m, _ptr(W), _ptr(Wq), _ptr(scale), _stream(self.device)),
+               "runlora_quantize_w_e4m3")
+        return QuantizedWeight(Wq, scale)
+
+    def forward_wq(self, fwd, shape, X, Wq, A, B, Y, ws=None):
+        ws = self.workspace(shape, True) if ws is None else ws
+        _check(_lib.runlora_forward_wq(self._h, int(fwd), C.byref(shape), _ptr(X), _ptr(Wq.q), _ptr(Wq.scale),
+                                       _ptr(A), _ptr(B), _ptr(Y), _ptr(ws), ws.numel(), _stream(self.device)),
+               "runlora_forward_wq")
+
+    def backward_wq(self, bwd, shape, X, Wq, A, B, dY, dX, dA, dB, accumulate=False, ws=None):
+        ws = self.workspace(shape, True) if ws is None else ws
+        _check(_lib.runlora_backward_wq(self._h, int(bwd), C.byref(shape), _ptr(X), _ptr(Wq.q), _ptr(Wq.scale),
+                                        _ptr(A), _ptr(B), _ptr(dY), _ptr(dX), _ptr(dA), _ptr(dB), _DT[dA.dtype],
+                                        int(bool(accumulate)), _ptr(ws), ws.numel(), _stream(self.device)),
+               "runlora_backward_wq")
 
     def select(self, shape: Shape, criterion=BY_FLOPS, ops: dict | None = None, grad_dtype=F32) -> Plan:
         p = Plan()
