@@ -56,35 +56,58 @@ __global__ void __launch_bounds__(256) finalize_scale_kernel(float* __restrict__
   if (j < m) scale[j] = col_scale(scale[j]);  // amax bits (as float) -> scale
 }
 
+// Each thread owns one group of `per` (16, or 8 when m % 16 != 0) columns — its scales stay
+// in registers — and walks the rows with a stride of (threads / column groups).
 __global__ void __launch_bounds__(256) dequantize_kernel(const uint8_t* __restrict__ Wq, const float* __restrict__ scale,
-                                                         int64_t k, int64_t m, __nv_bfloat16* __restrict__ W) {
+                                                         int64_t k, int64_t m, __nv_bfloat16* __restrict__ W,
+                                                         unsigned long long* lt) {
+  if (threadIdx.x == 0) ltrace_mark(lt, 0);
   pdl_wait();
   pdl_launch_dependents();
-  // 16 elements (16 bytes in, 32 bytes out) per thread and iteration when m % 16 == 0, else 8
+  if (threadIdx.x == 0) ltrace_mark(lt, 1);
   const int per = (m & 15) ? 8 : 16;
-  const int64_t groups = m / per, total = k * groups;
-  for (int64_t g = blockIdx.x * 256ll + threadIdx.x; g < total; g += (int64_t)gridDim.x * 256) {
-    const int64_t i = g / groups, j0 = (g % groups) * per;
-    uint8_t q[16];
-    if (per == 16) *reinterpret_cast<uint4*>(q) = __ldg(reinterpret_cast<const uint4*>(Wq + i * m + j0));
-    else *reinterpret_cast<uint2*>(q) = __ldg(reinterpret_cast<const uint2*>(Wq + i * m + j0));
+  const int64_t groups = m / per;
+  const int64_t tid = blockIdx.x * 256ll + threadIdx.x, nthr = (int64_t)gridDim.x * 256;
+  const int64_t rstride = nthr / groups;
+  if (rstride > 0 && tid < rstride * groups) {
+    const int64_t j0 = (tid % groups) * per;
+    float s[16];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (h * 8 >= per) break;
-      const float4 s0 = __ldg(reinterpret_cast<const float4*>(scale + j0 + 8 * h));
-      const float4 s1 = __ldg(reinterpret_cast<const float4*>(scale + j0 + 8 * h + 4));
-      const float s[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-      uint4 out;
-      __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(&out);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float a = __half2float(__half(__nv_cvt_fp8_to_halfraw(q[8 * h + 2 * e], __NV_E4M3))) * s[2 * e];
-        const float b = __half2float(__half(__nv_cvt_fp8_to_halfraw(q[8 * h + 2 * e + 1], __NV_E4M3))) * s[2 * e + 1];
-        o[e] = __floats2bfloat162_rn(a, b);
+    for (int e = 0; e < 16; e += 4) {
+      if (e < per) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(scale + j0 + e));
+        s[e] = v.x, s[e + 1] = v.y, s[e + 2] = v.z, s[e + 3] = v.w;
       }
-      *reinterpret_cast<uint4*>(W + i * m + j0 + 8 * h) = out;
+    }
+    for (int64_t i = tid / groups; i < k; i += rstride) {
+      uint8_t q[16];
+      if (per == 16) *reinterpret_cast<uint4*>(q) = __ldg(reinterpret_cast<const uint4*>(Wq + i * m + j0));
+      else *reinterpret_cast<uint2*>(q) = __ldg(reinterpret_cast<const uint2*>(Wq + i * m + j0));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h * 8 >= per) break;
+        uint4 out;
+        __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(&out);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c = 8 * h + 2 * e;
+          const float x0 = __half2float(__half(__nv_cvt_fp8_to_halfraw(q[c], __NV_E4M3))) * s[c];
+          const float x1 = __half2float(__half(__nv_cvt_fp8_to_halfraw(q[c + 1], __NV_E4M3))) * s[c + 1];
+          o[e] = __floats2bfloat162_rn(x0, x1);
+        }
+        *reinterpret_cast<uint4*>(W + i * m + j0 + 8 * h) = out;
+      }
+    }
+  } else if (rstride == 0) {  // more column groups than threads: grid-stride over everything
+    for (int64_t g = tid; g < k * groups; g += nthr) {
+      const int64_t i = g / groups, j0 = (g % groups) * per;
+      for (int e = 0; e < per; ++e) {
+        const float x = __half2float(__half(__nv_cvt_fp8_to_halfraw(Wq[i * m + j0 + e], __NV_E4M3))) * scale[j0 + e];
+        W[i * m + j0 + e] = __float2bfloat16_rn(x);
+      }
     }
   }
+  if (threadIdx.x == 0) ltrace_mark(lt, 2);
 }
 
 template <typename... KArgs, typename... Args>
@@ -105,7 +128,8 @@ cudaError_t launch(Ctx& ctx, KernelId kid, void (*kern)(KArgs...), dim3 grid, cu
 }
 
 unsigned elem_blocks(Ctx& ctx, int64_t total_threads) {
-  const int64_t b = (total_threads + 255) / 256, cap = (int64_t)ctx.num_sms() * 16;
+  // one resident wave (4 blocks of 256 threads per SM, any register count up to 64), grid-stride beyond it
+  const int64_t b = (total_threads + 255) / 256, cap = (int64_t)ctx.num_sms() * 4;
   return (unsigned)(b < cap ? (b > 0 ? b : 1) : cap);
 }
 
@@ -129,7 +153,8 @@ cudaError_t launch_quantize_w(Ctx& ctx, const void* W, int64_t k, int64_t m, voi
 cudaError_t launch_dequantize_w(Ctx& ctx, const void* Wq, const float* scale, int64_t k, int64_t m, void* W,
                                 cudaStream_t s) {
   return launch(ctx, KID_DEQUANT, dequantize_kernel, dim3(elem_blocks(ctx, k * (m / ((m & 15) ? 8 : 16)))), s,
-                static_cast<const uint8_t*>(Wq), scale, k, m, static_cast<__nv_bfloat16*>(W));
+                static_cast<const uint8_t*>(Wq), scale, k, m, static_cast<__nv_bfloat16*>(W),
+                ctx.ltrace_slot(KID_DEQUANT));
 }
 
 }  // namespace runlora

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--show", type=int, default=2)
     ap.add_argument("--shape", default=None, help="n,k,m (default: C2, n=8192, k=m=4096)")
+    ap.add_argument("--wq", action="store_true", help="quantized W (FP8 E4M3) entry points")
     a = ap.parse_args()
     assert os.environ.get("RUNLORA_LTRACE"), "set RUNLORA_LTRACE=1"
     c = synth.C2[a.r]
@@ -49,10 +50,18 @@ def main():
     buf = np.zeros(8 * 4096, dtype=np.uint64)
     kids = np.zeros(4096, dtype=np.int32)
 
+    qw = h.quantize_w(d["W"]) if a.wq else None
+    if a.wq:
+        ws = h.workspace(shape, True)
+
     def run(k):
         for _ in range(k):
-            h.forward(f, shape, d["X"], d["W"], d["A"], d["B"], Y, ws)
-            h.backward(b, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], dX, dA, dB, ws=ws)
+            if qw is not None:
+                h.forward_wq(f, shape, d["X"], qw, d["A"], d["B"], Y, ws)
+                h.backward_wq(b, shape, d["X"], qw, d["A"], d["B"], d["dY"], dX, dA, dB, ws=ws)
+            else:
+                h.forward(f, shape, d["X"], d["W"], d["A"], d["B"], Y, ws)
+                h.backward(b, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], dX, dA, dB, ws=ws)
 
     run(5)
     lib.runlora_debug_ltrace(h._h, buf.ctypes.data_as(C.POINTER(C.c_ulonglong)),
