@@ -34,23 +34,33 @@ LINEARS = ("q", "k", "v", "o", "gate", "up", "down")
 
 
 class LoRALinear(nn.Module):
-    """Frozen W [k, m] (paper orientation, Y = XW) with trainable A [k, r], B [r, m]."""
+    """Frozen W [k, m] (paper orientation, Y = XW) with trainable A [k, r], B [r, m].
+    ``quantize_()`` replaces W by its FP8 E4M3 form with per-column scales (QLoRA-style,
+    DESIGN.md R18); forward and backward then dequantize it per call."""
 
     def __init__(self, W: torch.Tensor, A: torch.Tensor, B: torch.Tensor):
         super().__init__()
         self.register_buffer("W", W)
         self.A = nn.Parameter(A)
         self.B = nn.Parameter(B)
+        self.wq: Optional[rl.QuantizedWeight] = None
+        self._km = tuple(W.shape)
         self.plan: Tuple[int, int] = (1, 1)
         self.sink: Optional[GradSink] = None
 
     @property
     def dims(self) -> Tuple[int, int, int]:
-        return self.W.shape[0], self.W.shape[1], self.A.shape[1]
+        return self._km[0], self._km[1], self.A.shape[1]
+
+    def quantize_(self) -> "LoRALinear":
+        self.wq = rl.handle(self.W.device).quantize_w(self.W)
+        self.W = None  # only the 8-bit weight and its scales stay resident
+        return self
 
     def forward(self, x):
         fwd, bwd = self.plan
-        return LoRALinearFunction.apply(x, self.W, self.A, self.B, fwd, bwd, self.sink)
+        return LoRALinearFunction.apply(x, self.wq if self.wq is not None else self.W, self.A, self.B, fwd, bwd,
+                                        self.sink)
 
 
 RMS_EPS = 1e-6
@@ -94,6 +104,12 @@ class LoRAStack(nn.Module):
         """(layer, name, module) in forward order."""
         return [(i, nm, L.lin[nm]) for i, L in enumerate(self.layers) for nm in LINEARS]
 
+    def quantize_(self) -> "LoRAStack":
+        """Every frozen W to FP8 E4M3 + per-column scales (QLoRA-style fine-tuning)."""
+        for _, _, lin in self.linears():
+            lin.quantize_()
+        return self
+
     def forward(self, x):
         for L in self.layers:
             x = L(x)
@@ -109,12 +125,13 @@ def plan_model(model: LoRAStack, n: int, criterion=rl.BY_FLOPS) -> Dict[Tuple[in
         k, m, r = lin.dims
         key = (k, m, r)
         if key not in plans:
-            shape = rl.make_shape(n, k, m, r, lin.W.dtype)
+            shape = rl.make_shape(n, k, m, r, lin.A.dtype)
             if criterion == rl.BY_FLOPS:
                 plans[key] = rl.select_by_flops(shape)
             else:
-                dev, dt = lin.W.device, lin.W.dtype
-                ops = {"X": torch.randn(n, k, device=dev, dtype=dt), "W": lin.W, "A": lin.A.detach(),
+                dev, dt = lin.A.device, lin.A.dtype
+                W = lin.W if lin.W is not None else torch.randn(k, m, device=dev, dtype=dt)  # timing stand-in
+                ops = {"X": torch.randn(n, k, device=dev, dtype=dt), "W": W, "A": lin.A.detach(),
                        "B": lin.B.detach(), "dY": torch.randn(n, m, device=dev, dtype=dt),
                        "Y": torch.empty(n, m, device=dev, dtype=dt), "dX": torch.empty(n, k, device=dev, dtype=dt),
                        "dA": torch.empty(k, r, device=dev), "dB": torch.empty(r, m, device=dev)}
@@ -176,7 +193,7 @@ class BucketedGradSync:
     def for_model(model: LoRAStack, **kw) -> "BucketedGradSync":
         """Attaches a sink to every linear of the model (backward order)."""
         lins = list(reversed(model.linears()))
-        sync = BucketedGradSync([(lin.dims, lin) for _, _, lin in lins], device=lins[0][2].W.device, **kw)
+        sync = BucketedGradSync([(lin.dims, lin) for _, _, lin in lins], device=lins[0][2].A.device, **kw)
         for s in sync.sinks:
             s.owner.sink = s
         return sync

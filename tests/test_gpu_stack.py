@@ -106,3 +106,32 @@ def test_stack_sinks_microbatched_time_plans(problem):
         errs[f"L{li}.{nm}.dB"] = rel_fro(_np(lin.sink.dB), grads_o[li][nm][1])
     bad = {k: e for k, e in errs.items() if not e <= TOL}
     assert not bad, (bad, errs)
+
+
+def test_stack_quantized_w_matches_oracle(problem):
+    """QLoRA-style stack (R18): every frozen W in FP8 E4M3 with column scales; the
+    oracle composition uses the same dequantized W~ (oracle/quant.py) in every linear."""
+    from oracle import quant as Q
+    from paper_2312_03415_b200 import runlora as rl
+    from paper_2312_03415_b200.stack import LoRAStack, plan_model
+    weights, x, dy, _, _, _ = problem
+    model = LoRAStack.from_weights(weights, "cuda").quantize_()
+    plan_model(model, N, rl.BY_FLOPS)
+    layers = []
+    for li, w in enumerate(weights):
+        L = {}
+        for nm in S.LINEARS:
+            lin = model.layers[li].lin[nm]
+            assert lin.W is None and lin.wq.q.dtype == torch.uint8
+            L[nm] = {"W": Q.dequantize_w(lin.wq.q.cpu().numpy(), lin.wq.scale.cpu().numpy()),
+                     "A": w[nm]["A"].double().numpy(), "B": w[nm]["B"].double().numpy()}
+        layers.append(L)
+    y_o, cache = S.stack_forward(x.double().numpy(), layers)
+    dx_o, grads_o = S.stack_backward(dy.double().numpy(), layers, cache)
+    xg = x.cuda().requires_grad_(True)
+    y = model(xg)
+    y.backward(dy.cuda())
+    torch.cuda.synchronize()
+    errs = _errors(y, xg, model.linears(), y_o, dx_o, grads_o)
+    bad = {k: e for k, e in errs.items() if not e <= TOL}
+    assert not bad, (bad, errs)
