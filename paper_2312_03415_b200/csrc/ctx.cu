@@ -25,6 +25,8 @@ Ctx::Ctx(int device) : device_(device) {
   if (const char* e = getenv("RUNLORA_OCC2")) occ2_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_PDL")) pdl_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_L2PROMO_MN")) promo_mn_ = (CUtensorMapL2promotion)atoi(e);
+  if (const char* e = getenv("RUNLORA_TMA_STORE_MAIN")) tma_store_main_ = atoi(e) != 0;
+  if (const char* e = getenv("RUNLORA_TMA_STORE_WPRIME")) tma_store_wprime_ = atoi(e) != 0;
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
@@ -45,8 +47,6 @@ Ctx::Ctx(int device) : device_(device) {
     if (cudaMalloc(&identity_, eye.size() * 2) != cudaSuccess ||
         cudaMemcpy(identity_, eye.data(), eye.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess) {
       if (identity_) cudaFree(identity_);
-  if (trace) cudaFree(trace);
-  if (ltrace_) cudaFree(ltrace_);
       identity_ = nullptr;
     }
   }
