@@ -8,12 +8,13 @@
 // bf16 operands, fp32 accumulation in TMEM.  Every bf16 product of the paper's
 // variants (Eq. 1-3, Alg. 1-5) is a problem of this kernel:
 //   * Y = [X | XA]·[W ; B]           (forward1 fused)   A K-major, B MN-major
-//   * Y = X·(W+AB)                   (forward2)          A K-major, B MN-major
+//   * Y = X·(W+AB)                   (forward2)          A K-major, B K-major (W'ᵀ)
 //   * dX = [dY | dYBᵀ]·[Wᵀ ; Aᵀ]     (Alg. 1-3 last line)      A K-major, B K-major
 //   * dX = dY·(W+AB)ᵀ                (Alg. 4-5 last line)      A K-major, B K-major
-//   * Z1 = dY·Bᵀ, Z2 = X·A           (rank-r projections)      N = r
-//   * dA = Xᵀ·Z1, dBᵀ = dYᵀ·Z2       (token reductions, K = n) A and B MN-major, split-K
-//   * W+AB                           (K = r, epilogue adds W)
+//   * Z1 = dY·Bᵀ, Z2 = X·A           (rank-r projections)      N = r; K-split bf16 blocks
+//   * dA = Xᵀ·Z1, dBᵀ = dYᵀ·Z2       (token reductions, K = n) A and B MN-major, split-K,
+//                                                              partial Z blocks folded
+//   * W+AB, (W+AB)ᵀ                  (K = r plus an identity tail that adds W, tail_diag)
 //
 // Structure (persistent, warp-specialised, one CTA per SM; CG = 2 pairs two SMs
 // of a cluster on one 256-row tile with tcgen05 cta_group::2):
@@ -21,9 +22,11 @@
 //   warp 1 lane 0 : tcgen05.mma issuer (leader CTA only)
 //   warp 2        : TMEM allocator (2 accumulators of BN_MAX columns: the epilogue of
 //                   tile i overlaps the mainloop of tile i+1)
-//   warps 4..7    : epilogue (tcgen05.ld -> registers -> global), TMEM lanes 32*(w%4)..
-// Tiles: 128 rows per CTA, bn columns (runtime, <= BN_MAX), BK = 64 (one 128-byte
-// swizzle row of bf16).  Shared-memory tiles use the 128B swizzle written by TMA:
+//   warps 4..7    : epilogue (tcgen05.ld -> registers -> global, or -> swizzled smem ->
+//                   TMA store for EPI = 3), TMEM lanes 32*(w%4)..
+// Tiles: 128 rows per CTA, bn columns (runtime, <= BN_MAX), K atoms of 64 (one 128-byte
+// swizzle row of bf16), KS atoms per pipeline stage.  Shared-memory tiles use the 128B
+// swizzle written by TMA:
 //   K-major  tile: rows of 128 B (64 K-elements), 8-row atoms of 1024 B  -> SBO = 1024
 //   MN-major tile: 64-element MN chunks, each a box of 64 K-rows x 128 B  -> LBO = 8192
 //                  (MN chunk stride), SBO = 1024 (8 K-rows); a UMMA_K=16 step is +2048 B.
