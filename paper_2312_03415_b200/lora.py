@@ -90,11 +90,21 @@ class LoRALinearFunction(torch.autograd.Function):
 
 
 def lora_linear(X, W, A, B, plan=None, criterion=rl.BY_FLOPS):
-    """Functional entry: selects the (forward, backward) pair for this shape (cached
-    per shape by the library for time-based criteria) and applies it."""
+    """Functional entry: selects the (forward, backward) pair for this shape and applies it.
+    BY_FLOPS: Table 1 (host only).  BY_TIME / HYBRID: the library times the candidates once
+    per shape on scratch operands of this shape (then serves the cached plan)."""
     if plan is None:
         shape = _shape(X, W, A)
-        plan = rl.select_by_flops(shape) if criterion == rl.BY_FLOPS else None
-        if plan is None:
-            raise ValueError("time-based selection needs operands: call Handle.select(..., ops=...) first")
+        if criterion == rl.BY_FLOPS:
+            plan = rl.select_by_flops(shape)
+        else:
+            n, k = X.shape
+            m, r = W.shape[1], A.shape[1]
+            dev, dt = X.device, X.dtype
+            Wt = torch.randn(k, m, device=dev, dtype=dt) if _is_q(W) else W  # timing stand-in
+            ops = {"X": X.detach(), "W": Wt, "A": A.detach(), "B": B.detach(),
+                   "dY": torch.randn(n, m, device=dev, dtype=dt), "Y": torch.empty(n, m, device=dev, dtype=dt),
+                   "dX": torch.empty(n, k, device=dev, dtype=dt),
+                   "dA": torch.empty(k, r, device=dev), "dB": torch.empty(r, m, device=dev)}
+            plan = rl.handle(dev).select(shape, criterion, ops=ops, grad_dtype=rl.F32)
     return LoRALinearFunction.apply(X, W, A, B, int(plan.fwd), int(plan.bwd))

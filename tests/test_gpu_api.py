@@ -194,3 +194,21 @@ def test_launch_timeline_records(rl, monkeypatch):
     assert np.all(rec[:, 0] <= rec[:, 1]) and np.all(rec[:, 1] <= rec[:, 2]) and np.all(rec[:, 2] <= rec[:, 4])
     assert np.all(rec[:, 3] <= rec[:, 4])
     assert np.all(np.diff(rec[:, 1]) > 0)  # PDL: each launch becomes ready after its predecessor
+
+
+def test_lora_linear_time_criterion(rl):
+    """The functional entry times the candidates once per shape and applies the plan."""
+    from paper_2312_03415_b200.lora import lora_linear
+    c = synth.case("fn_time", 0, 26, 768, 512, 640, 16, "bf16")
+    ops = synth.operands(c)
+    X = ops["X"].cuda().requires_grad_(True)
+    A = ops["A"].cuda().requires_grad_(True)
+    B = ops["B"].cuda().requires_grad_(True)
+    Y = lora_linear(X, ops["W"].cuda(), A, B, criterion=rl.BY_TIME)
+    Y.backward(ops["dY"].cuda())
+    torch.cuda.synchronize()
+    Xn, Wn, An, Bn, dYn = (_np(ops[k]) for k in ("X", "W", "A", "B", "dY"))
+    wA, wB, wX = O.reference_backward(Xn, Wn, An, Bn, dYn)
+    assert O.rel_fro(_np(Y), O.forward(1, Xn, Wn, An, Bn)) <= TOL
+    for g, w in ((A.grad, wA), (B.grad, wB), (X.grad, wX)):
+        assert O.rel_fro(_np(g), w) <= TOL
