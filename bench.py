@@ -218,6 +218,10 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        # 6 main-GEMM stages leave shared memory for NCCL's kernels, which then co-reside
+        # with the dX GEMM that the adapter-gradient allreduce overlaps
+        os.environ.setdefault("RUNLORA_MAIN_STAGES", "6")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)

@@ -96,6 +96,11 @@ class Ctx {
   int trace_kid = -1;
   static constexpr int kTraceUnits = 1 << 16;  // == kTraceMaxUnits (tc_gemm.cuh); + 4 words per CTA
   bool tma_store_main() const { return tma_store_main_; }
+  // main-GEMM pipeline stages (env RUNLORA_MAIN_STAGES; 0 = all that fit = 7).  6 stages
+  // cost ~1 % in a step (the GEMM alone: 166.9 µs either way; 5: 169, 4: 181) and leave
+  // 32 KB of shared memory per SM, so NCCL's kernels can co-reside with the dX GEMM that
+  // the data-parallel allreduce overlaps (bench.py sets 6 when it runs more than one rank).
+  int main_stages() const { return main_stages_; }
   bool tma_store_wprime() const { return tma_store_wprime_; }
 
   // Encodes (or fetches from cache) a 2-D bf16 TMA descriptor with swz_bytes swizzle
@@ -128,6 +133,7 @@ class Ctx {
   int main_cg_ = 2;
   void* identity_ = nullptr;
   bool tma_store_main_ = false;   // env RUNLORA_TMA_STORE_MAIN=1
+  int main_stages_ = 0;
   bool tma_store_wprime_ = true;  // env RUNLORA_TMA_STORE_WPRIME=0
   bool occ2_ = true;
   bool pdl_ = true;

@@ -41,11 +41,14 @@ cudaError_t launch_pdl(Ctx& ctx, void (*kern)(KArgs...), dim3 grid, dim3 block, 
 template <int BN, int CG, int OCC = 1, int EPI = 0, int KS = 1>
 cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, GemmArgs& g, cudaStream_t s) {
   auto kern = tc_gemm_kernel<BN, CG, OCC, EPI, KS>;
-  constexpr uint32_t smem = TileCfg<BN, CG, OCC, EPI, KS>::SMEM_BYTES;
+  using TC = TileCfg<BN, CG, OCC, EPI, KS>;
+  constexpr uint32_t smem_max = TC::SMEM_BYTES;
+  const int stages = (g.stages > 0 && g.stages < TC::STAGES) ? g.stages : TC::STAGES;
+  const uint32_t smem = smem_max - (uint32_t)(TC::STAGES - stages) * TC::STAGE_BYTES;
   static bool attr_set[kMaxDevices] = {};
   const int dev = ctx.device();
   if (dev < kMaxDevices && !attr_set[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
     if (e != cudaSuccess) return e;
     // the whole unified L1/shared array as shared memory, so OCC = 2 CTAs are co-resident
     e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -352,6 +355,7 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
   g.nprob = nreq;
   g.trace = (ctx.trace && ctx.trace_kid == reqs[0].kid && g.total_units <= Ctx::kTraceUnits) ? ctx.trace : nullptr;
   g.ltrace = ctx.ltrace_slot(reqs[0].kid);
+  g.stages = reqs[0].kid == KID_GEMM_MAIN ? ctx.main_stages() : 0;
   if (const char* d = getenv("RUNLORA_DBG_GEMM")) g.dbg = atoi(d);
   for (int q = nreq; q < kMaxProb; ++q) g.p[q] = g.p[0], g.p[q].units = 0;
   if (g.total_units <= 0) return cudaSuccess;

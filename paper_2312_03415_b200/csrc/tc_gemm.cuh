@@ -87,6 +87,7 @@ struct GemmArgs {
   // issued, 3: epilogue done, 4: CTA, 5: problem}] (%globaltimer ns).
   unsigned long long* trace;
   unsigned long long* ltrace;  // launch timeline slot (nullptr: off)
+  int stages;                  // pipeline stages (0: the compiled maximum TileCfg::STAGES)
 };
 
 struct Tmaps {  // per problem: A1, B1, A2, B2, D (EPI = 3: TMA-store epilogue)
@@ -211,7 +212,9 @@ template <int BN_MAX, int CG, int OCC = 1, int EPI = 0, int KS = 1>
 __global__ void __launch_bounds__(kGemmThreads, OCC)
     tc_gemm_kernel(const __grid_constant__ Tmaps tm, const __grid_constant__ GemmArgs g) {
   using C = TileCfg<BN_MAX, CG, OCC, EPI, KS>;
-  constexpr int STAGES = C::STAGES;
+  // runtime ring depth <= the compiled maximum (fewer stages leave shared memory to kernels
+  // that should co-reside, e.g. NCCL's during an overlapped allreduce)
+  const int STAGES = (g.stages > 0 && g.stages < C::STAGES) ? g.stages : C::STAGES;
   static_assert(BN_MAX % (16 * CG) == 0 && BN_MAX >= 16 && BN_MAX <= 256, "UMMA N");
 
   extern __shared__ uint8_t smem_raw[];
