@@ -19,6 +19,11 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+__device__ __forceinline__ unsigned smid() {
+  unsigned v;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(v));
+  return v;
+}
 // Launch timeline slot (Ctx::ltrace_slot): phase 0 = CTA entry, 1 = ready (after the PDL
 // wait), 2 = CTA exit.  Called by one thread per CTA.
 __device__ __forceinline__ void ltrace_mark(unsigned long long* lt, int phase) {

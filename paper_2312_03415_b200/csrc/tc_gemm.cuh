@@ -82,7 +82,9 @@ struct GemmArgs {
   Prob p[kMaxProb];
   int nprob;
   int total_units;
-  int dbg;  // 0 normal; 1: no TMA (MMA-only); 2: no MMA (TMA-only); 3: as 1 + no stores; 4: as 1 + no epilogue
+  int dbg;  // 0 normal; 1: no TMA (MMA-only); 2: no MMA (TMA-only); 3: as 1 + no stores; 4: as 1 + no epilogue;
+            // 5: A loads only (MMA on stale B); 6: B loads only (stale A); 7: A loads on even
+            // k-blocks only (75 % of the TMA bytes)
   // Debug timeline (RUNLORA_TRACE): per unit u, trace[8u + {0: producer start, 2: last load
   // issued, 3: epilogue done, 4: CTA, 5: problem}] (%globaltimer ns).
   unsigned long long* trace;
@@ -233,9 +235,9 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
   const int group = blockIdx.x / CG;
   const int ngroups = gridDim.x / CG;
 
-  // debug timeline per CTA (after the units): {kernel entry, inputs ready (after PDL wait), exit}
+  // debug timeline per CTA (after the units): {kernel entry, inputs ready (after PDL wait), exit, SM id}
   unsigned long long* ctrace = g.trace ? g.trace + 8ull * kTraceMaxUnits + 4ull * blockIdx.x : nullptr;
-  if (ctrace && threadIdx.x == 0) ctrace[0] = globaltimer();
+  if (ctrace && threadIdx.x == 0) ctrace[0] = globaltimer(), ctrace[3] = smid();
   if (threadIdx.x == 0) ltrace_mark(g.ltrace, 0);
   if (warp == 0 && lane == 0) {
     for (int q = 0; q < g.nprob; ++q)
@@ -290,7 +292,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       // snake: every other round of this CTA walks K backwards, starting where the data it
       // (and its neighbours) just streamed is still in L2
       const bool rev = p.snake && (i_u & 1);
-      if (g.dbg == 1 || g.dbg >= 3) continue;
+      if (g.dbg == 1 || g.dbg == 3 || g.dbg == 4) continue;
       const int cw = p.b_swz >> 1;   // MN-major B chunk width (elements)
       const int cb = p.b_swz * kBK;  // MN-major B chunk bytes (64 K-rows)
       for (int i0 = 0; i0 < nkb; i0 += KS) {
@@ -298,7 +300,10 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
         if (elect_one_sync()) {
           const int natoms = min(KS, nkb - i0);
           uint64_t* fb = &full[stage];
-          if (leader) mbar_arrive_expect_tx(fb, p.stage_tx * (uint32_t)natoms);
+          const bool skip_a = g.dbg == 6 || (g.dbg == 7 && (i0 & 1));
+          const uint32_t tx = g.dbg == 5 ? (uint32_t)(CG * kBM * kBK * 2)
+                              : skip_a ? p.stage_tx - (uint32_t)(CG * kBM * kBK * 2) : p.stage_tx;
+          if (leader) mbar_arrive_expect_tx(fb, tx * (uint32_t)natoms);
           for (int at = 0; at < natoms; ++at) {
             const int i = i0 + at;
             uint8_t* a = sA + stage * C::A_BYTES + at * C::A_ATOM;
@@ -311,7 +316,8 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
             const int kc = (tail ? (i - nmain) : (kb0 + ki)) * kBK;
             const int ma = diag ? 0 : m0;          // identity tail: rows of I
             const int kcb = diag ? m0 + kc : kc;   // identity tail: B2 rows of this tile
-            if (!p.a_mn) {
+            if (skip_a) {
+            } else if (!p.a_mn) {
               tma_load_2d<CG>(ta, fb, a, kc, ma, p.hint_a);
             } else if (p.a_3d) {
               tma_load_3d<CG>(ta, fb, a, 0, kc, ma >> 6, p.hint_a);
@@ -319,7 +325,8 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
               tma_load_2d<CG>(ta, fb, a, ma, kc, p.hint_a);
               tma_load_2d<CG>(ta, fb, a + 8192, ma + 64, kc, p.hint_a);
             }
-            if (!p.b_mn) {
+            if (g.dbg == 5) {
+            } else if (!p.b_mn) {
               tma_load_2d<CG>(tb, fb, b, kcb, n0, p.hint_b);
             } else if (p.b_3d) {
               tma_load_3d<CG>(tb, fb, b, 0, kcb, n0 / cw, p.hint_b);
@@ -365,7 +372,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       const uint64_t a_hi = smem_desc(0, p.a_mn ? 8192 : 16, 1024, 2u);
       const uint64_t b_hi = smem_desc(0, p.b_mn ? 64u * b_swz : 16u, 8u * b_swz, sw_layout_code(b_swz));
       for (int i0 = 0; i0 < nkb; i0 += KS) {
-        if (g.dbg != 1 && g.dbg < 3) mbar_wait(&full[stage], phase);
+        if (g.dbg != 1 && g.dbg != 3 && g.dbg != 4) mbar_wait(&full[stage], phase);
         tc_fence_after();
         const int natoms = min(KS, nkb - i0);
         if (elect_one_sync()) {

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--plan", default="2,1")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--show", type=int, default=2)
+    ap.add_argument("--warm", type=int, default=5, help="untimed steps first (1000+: power-capped clocks)")
     ap.add_argument("--shape", default=None, help="n,k,m (default: C2, n=8192, k=m=4096)")
     ap.add_argument("--wq", action="store_true", help="quantized W (FP8 E4M3) entry points")
     a = ap.parse_args()
@@ -63,7 +64,7 @@ def main():
                 h.forward(f, shape, d["X"], d["W"], d["A"], d["B"], Y, ws)
                 h.backward(b, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], dX, dA, dB, ws=ws)
 
-    run(5)
+    run(a.warm)
     lib.runlora_debug_ltrace(h._h, buf.ctypes.data_as(C.POINTER(C.c_ulonglong)),
                              kids.ctypes.data_as(C.POINTER(C.c_int)), 4096)  # reset
     torch.cuda.synchronize()

@@ -51,6 +51,16 @@ if len(ct):
           f"{(ct[:, 1].min() - k0) / 1e3:.1f}..{(ct[:, 1].max() - k0) / 1e3:.1f}, first unit {(t0 - k0) / 1e3:.1f}, "
           f"last unit done {(t[:, 3].max() - k0) / 1e3:.1f}, CTA exit {(ct[:, 2].min() - k0) / 1e3:.1f}.."
           f"{(ct[:, 2].max() - k0) / 1e3:.1f} us")
+    # exit time by the number of this launch's CTAs co-resident on the SM
+    sm = ct[:, 3]
+    cnt = {v: (sm == v).sum() for v in np.unique(sm)}
+    per = np.array([cnt[v] for v in sm])
+    ex = (ct[:, 2] - ct[:, 1].min()) / 1e3
+    for c_ in np.unique(per):
+        sel = per == c_
+        print(f"  CTAs on an SM = {c_}: {sel.sum():4d} CTAs on {len([v for v in cnt if cnt[v] == c_])} SMs, "
+              f"exit after ready med {np.median(ex[sel]):6.1f} min {ex[sel].min():6.1f} max {ex[sel].max():6.1f} us")
+    print(f"  SMs used {len(cnt)}")
 for q in np.unique(t[:, 5]):
     s = t[:, 5] == q
     wait = T[s, 1] - T[s, 0]
