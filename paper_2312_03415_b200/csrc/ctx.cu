@@ -27,6 +27,11 @@ Ctx::Ctx(int device) : device_(device) {
   if (const char* e = getenv("RUNLORA_L2PROMO_MN")) promo_mn_ = (CUtensorMapL2promotion)atoi(e);
   if (const char* e = getenv("RUNLORA_MAIN_STAGES")) main_stages_ = atoi(e) > 0 ? atoi(e) : 0;  // 0: all
   if (const char* e = getenv("RUNLORA_TMA_STORE_MAIN")) tma_store_main_ = atoi(e) != 0;
+  if (const char* e = getenv("RUNLORA_MAIN_WIDE")) main_wide_ = atoi(e) != 0;
+  if (const char* e = getenv("RUNLORA_WIDE_COST")) {
+    double b = 0, sm = 0;
+    if (sscanf(e, "%lf,%lf", &b, &sm) == 2 && b > 0 && sm > 0) wide_cost_big_ = b, wide_cost_small_ = sm;
+  }
   if (const char* e = getenv("RUNLORA_TMA_STORE_WPRIME")) tma_store_wprime_ = atoi(e) != 0;
   int prev = -1;
   cudaGetDevice(&prev);

@@ -96,6 +96,11 @@ class Ctx {
   int trace_kid = -1;
   static constexpr int kTraceUnits = 1 << 16;  // == kTraceMaxUnits (tc_gemm.cuh); + 4 words per CTA
   bool tma_store_main() const { return tma_store_main_; }
+  // 512-wide pair tiles for the main GEMMs (env RUNLORA_MAIN_WIDE=0 disables); unit costs of
+  // the planner (env RUNLORA_WIDE_COST="big,small", in MMA-only 256x256 tile times)
+  bool main_wide() const { return main_wide_; }
+  double wide_cost_big() const { return wide_cost_big_; }
+  double wide_cost_small() const { return wide_cost_small_; }
   // main-GEMM pipeline stages (env RUNLORA_MAIN_STAGES; 0 = all that fit = 7).  6 stages
   // cost ~1 % in a step (the GEMM alone: 166.9 µs either way; 5: 169, 4: 181) and leave
   // 32 KB of shared memory per SM, so NCCL's kernels can co-reside with the dX GEMM that
@@ -133,6 +138,8 @@ class Ctx {
   int main_cg_ = 2;
   void* identity_ = nullptr;
   bool tma_store_main_ = false;   // env RUNLORA_TMA_STORE_MAIN=1
+  bool main_wide_ = true;
+  double wide_cost_big_ = 2.2, wide_cost_small_ = 1.33;
   int main_stages_ = 0;
   bool tma_store_wprime_ = true;  // env RUNLORA_TMA_STORE_WPRIME=0
   bool occ2_ = true;
@@ -174,6 +181,8 @@ class Ctx {
 };
 
 // Kernel launchers (kernels.cu). Return cudaSuccess or the launch error.
+// Row tiles per raster band of a tc_gemm problem (decode_unit in tc_gemm.cuh).
+int raster_rows(const GemmReq& r);
 cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t s, std::string* err);
 // Fixed-order sum of fp32 split-K slabs P[split][rows][ldp] (first `cols` columns) into
 // out (fp32 or bf16; optionally transposed: out[j*ldo + i]; optionally accumulated).

@@ -94,6 +94,7 @@ cudaError_t dispatch_tc(Ctx& ctx, int bn_max, int cg, bool occ2, bool tma_store,
   if (tma_store) {
     if (cg == 1 && bn_max == 256) return run_tc<256, 1, 1, 3>(ctx, tm, g, s);
     if (cg == 2 && bn_max == 256) return run_tc<256, 2, 1, 3>(ctx, tm, g, s);
+    if (cg == 2 && bn_max == 512) return run_tc<512, 2, 1, 3>(ctx, tm, g, s);
     return cudaErrorNotSupported;
   }
   if (cg == 2) {
@@ -102,6 +103,7 @@ cudaError_t dispatch_tc(Ctx& ctx, int bn_max, int cg, bool occ2, bool tma_store,
     // (8192x4096x4096: 180 vs 197 µs) and neutral for K-major operands (168 µs both).
     static const int ks_env = getenv("RUNLORA_MAIN_KS") ? atoi(getenv("RUNLORA_MAIN_KS")) : 0;
     const bool ks2 = ks_env ? ks_env == 2 : (g.p[0].a_mn || g.p[0].b_mn);
+    if (bn_max == 512) return run_tc<512, 2>(ctx, tm, g, s);
     if (bn_max == 256 && ks2) return run_tc<256, 2, 1, 0, 2>(ctx, tm, g, s);
     if (bn_max == 256) return run_tc<256, 2>(ctx, tm, g, s);
     if (bn_max == 128) return run_tc<128, 2>(ctx, tm, g, s);
@@ -262,6 +264,13 @@ __global__ void __launch_bounds__(256) sgemm_kernel(int M, int N, int K, const f
 
 }  // namespace
 
+int raster_rows(const GemmReq& r) {
+  // all of B (N x K bf16) above ~48 MB -> banded raster (see decode_unit); env RUNLORA_RASTER_G
+  static const int raster_env = getenv("RUNLORA_RASTER_G") ? atoi(getenv("RUNLORA_RASTER_G")) : 0;
+  const double b_bytes = 2.0 * (double)r.N * (double)(r.K1 + r.K2);
+  return raster_env > 0 ? raster_env : b_bytes > 48e6 ? 8 : 1;
+}
+
 cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t s, std::string* err) {
   if (nreq < 1 || nreq > kMaxProb) return cudaErrorInvalidValue;
   Tmaps tm;
@@ -273,12 +282,17 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
   for (int q = 0; q < nreq; ++q) {
     const GemmReq& r = reqs[q];
     if ((r.cg > 1 ? 2 : 1) != cg || r.tma_store != tma_store) return cudaErrorInvalidValue;
-    if (r.tma_store && (r.out_mode != OUT_BF16 || r.BN != 256 || r.splits > 1)) {
-      if (err) *err = "tc_gemm: TMA-store epilogue needs a plain bf16 output with 256-wide tiles";
+    if (r.BN > 256 && (r.BN != 512 || cg != 2 || r.b_mn || r.splits > 1 || r.tail_diag ||
+                       !(r.out_mode == OUT_BF16 || r.out_mode == OUT_F32))) {
+      if (err) *err = "tc_gemm: 512-wide tiles need a CTA pair, K-major B and a plain output";
+      return cudaErrorInvalidValue;
+    }
+    if (r.tma_store && (r.out_mode != OUT_BF16 || r.BN < 256 || r.splits > 1)) {
+      if (err) *err = "tc_gemm: TMA-store epilogue needs a plain bf16 output with 256- or 512-wide tiles";
       return cudaErrorInvalidValue;
     }
     // MN-major B: 128B swizzle in 64-column chunks, or one 16/32-column chunk (32B/64B swizzle)
-    const int nb = r.BN / cg;
+    const int nb = std::min(r.BN, 256) / cg;  // B columns per CTA and MMA (512-wide: two MMAs)
     const int b_swz = !r.b_mn ? 128 : (nb % 64 == 0 ? 128 : nb == 32 ? 64 : nb == 16 ? 32 : 0);
     if (r.BN % (16 * cg) != 0 || b_swz == 0) {
       if (err) *err = "tc_gemm: illegal tile width for operand majorness";
@@ -326,12 +340,10 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
     p.a_3d = a3 ? 1 : 0;
     static const bool snake = getenv("RUNLORA_SNAKE") == nullptr || atoi(getenv("RUNLORA_SNAKE")) != 0;
     p.snake = (snake && r.splits <= 1 && r.kid == KID_GEMM_MAIN) ? 1 : 0;
-    // all of B (N x K bf16) above ~48 MB -> banded raster (see decode_unit)
-    const double b_bytes = 2.0 * (double)r.N * (double)(r.K1 + r.K2);
-    p.raster_g = b_bytes > 48e6 ? 8 : 1;
+    p.raster_g = raster_rows(r);
     p.b_3d = b3 ? 1 : 0;
     p.out_mode = r.out_mode;
-    p.idesc = idesc_bf16(kBM * cg, r.BN, r.a_mn, r.b_mn);
+    p.idesc = idesc_bf16(kBM * cg, std::min(r.BN, 256), r.a_mn, r.b_mn);
     p.stage_tx = (uint32_t)cg * (uint32_t)(kBM * kBK * 2 + (r.BN / cg) * kBK * 2);
     p.D = r.D;
     p.ldd = r.ldd;

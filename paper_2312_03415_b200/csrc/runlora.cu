@@ -522,11 +522,96 @@ runlora_status_t wprime_t_bf16(Ctx& c, const runlora_shape_t& s, const void* W, 
   return gemm(c, q, st);
 }
 
+// ------------------------------------------------------------ 512-wide main-GEMM tiles
+// A 256x512 pair tile (two N = 256 MMAs per k-step sharing the A tile) moves 25 % fewer TMA
+// bytes per FLOP than a 256x256 one; the main GEMM's time tracks those bytes,
+// but the tile's 512 accumulator columns leave no second TMEM buffer, so its epilogue is
+// exposed, and big tiles quantise badly on 74 pairs (C2: 256 tiles = 3.46 rounds).  So the
+// output rows [0, rows_big) run as 512-wide tiles and the rest as 256-wide ones in the same
+// launch (two problems); rows_big minimises the busiest pair's summed unit cost under the
+// kernel's static round-robin assignment (unit u -> pair u mod 74), costs in units of an
+// MMA-only 256x256 tile (measured: big 2.2 incl. the exposed epilogue, small 1.33).
+struct WideSplit {
+  int rows_big;  // multiple of 256; 0 = no 512-wide tiles
+  double cost, cost_small_only;
+};
+
+// decode_unit's raster (tc_gemm.cuh) on the host: unit -> (row tile, column tile)
+static void host_unit_tile(int u, int mt, int nt, int G, int* m_blk, int* n_blk) {
+  const int band = u / (G * nt);
+  const int m_first = band * G;
+  const int g_rows = std::min(G, mt - m_first);
+  const int r = u - band * G * nt;
+  *m_blk = m_first + r % g_rows;
+  *n_blk = r / g_rows;
+}
+
+WideSplit wide_split(const Ctx& c, const GemmReq& q) {
+  WideSplit w{0, 0, 0};
+  const int pairs = c.num_sms() / 2;
+  const int mt = (q.M + 255) / 256;
+  const int ntb = (q.N + 511) / 512, nts = (q.N + 255) / 256;
+  const bool ragged = (int64_t)ntb * 512 - q.N >= 256;  // last 512-wide column tile has one half
+  const double cb = c.wide_cost_big(), cs = c.wide_cost_small();
+  const int G = raster_rows(q);
+  std::vector<double> load(pairs);
+  auto simulate = [&](int rb) {
+    std::fill(load.begin(), load.end(), 0.0);
+    const int ub = rb * ntb, us = (mt - rb) * nts;
+    for (int u = 0; u < ub; ++u) {
+      int mb, nb;
+      host_unit_tile(u, rb, ntb, G, &mb, &nb);
+      load[u % pairs] += (ragged && nb == ntb - 1) ? cs : cb;
+    }
+    for (int u = 0; u < us; ++u) load[(ub + u) % pairs] += cs;
+    return *std::max_element(load.begin(), load.end());
+  };
+  w.cost_small_only = simulate(0);
+  w.cost = w.cost_small_only;
+  if (!c.main_wide() || q.cg != 2 || q.a_mn || q.b_mn || q.splits > 1 || q.out_mode != OUT_BF16) return w;
+  for (int rb = 1; rb <= mt; ++rb) {
+    const double t = simulate(rb);
+    if (t < w.cost * 0.995) w.cost = t, w.rows_big = rb * 256;
+  }
+  return w;
+}
+
+static DeviceMat rows_from(const DeviceMat& m, int64_t r0) {
+  return DeviceMat{static_cast<const char*>(m.ptr) + r0 * m.ld * 2, m.rows - r0, m.cols, m.ld};
+}
+
 // Runs a main GEMM (bf16 D = q.D, ld q.ldd), split over K into fp32 slabs in the P region
-// and reduced when main_split says so.
+// and reduced when main_split says so, or as 512-/256-wide tiles when wide_split says so.
 runlora_status_t main_gemm(Ctx& c, GemmReq q, Bufs& b, cudaStream_t st) {
   const MainSplit ms = main_split(q.M, q.N, q.K1);
-  if (ms.splits <= 1) return gemm(c, q, st);
+  if (ms.splits <= 1) {
+    const WideSplit w = wide_split(c, q);
+    static const bool dbg = getenv("RUNLORA_DEBUG_WIDE") != nullptr;
+    if (dbg)
+      fprintf(stderr, "[runlora] main GEMM %dx%dx%d: 512-wide rows %d, est. %.2f vs %.2f (256-wide only)\n", q.M, q.N,
+              q.K1 + q.K2, w.rows_big, w.cost, w.cost_small_only);
+    if (w.rows_big == 0) return gemm(c, q, st);
+    GemmReq r[2] = {q, q};
+    const int rb = std::min(w.rows_big, q.M);
+    r[0].BN = 512;
+    r[0].M = rb;
+    r[0].a.rows = rb;
+    if (r[0].K2 > 0) r[0].a2.rows = rb;
+    r[0].tma_store = true;  // the exposed epilogue: full-line bulk stores
+    int nreq = 1;
+    if (rb < q.M) {
+      r[1].M = q.M - rb;
+      r[1].a = rows_from(q.a, rb);
+      if (q.K2 > 0) r[1].a2 = rows_from(q.a2, rb);
+      r[1].D = static_cast<char*>(q.D) + (int64_t)rb * q.ldd * 2;
+      r[1].tma_store = true;
+      nreq = 2;
+    }
+    std::string err;
+    cudaError_t e = launch_tc_gemm(c, r, nreq, st, &err);
+    if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
+    return RUNLORA_OK;
+  }
   void* out = q.D;
   const int64_t ldo = q.ldd;
   q.out_mode = OUT_F32;
@@ -1302,6 +1387,8 @@ extern "C" runlora_status_t runlora_debug_gemm(runlora_handle_t h, int M, int N,
   q.kb_per_split = (nk + splits - 1) / splits;
   q.splits = (nk + q.kb_per_split - 1) / q.kb_per_split;
   q.split_stride = (int64_t)M * N;
+  // env RUNLORA_DEBUG_TMA_STORE=1: the TMA-store epilogue (plain bf16 output, 256/512-wide tiles)
+  q.tma_store = getenv("RUNLORA_DEBUG_TMA_STORE") && out_mode == OUT_BF16 && q.splits <= 1 && BN >= 256;
   DeviceGuard dg(h->ctx->device());
   RL_TRY(gemm(*h->ctx, q, static_cast<cudaStream_t>(stream)));
   return post_launch();

@@ -20,8 +20,9 @@
 // of a cluster on one 256-row tile with tcgen05 cta_group::2):
 //   warp 0 lane 0 : TMA producer (smem ring of STAGES {A,B} tiles, mbarrier full/empty)
 //   warp 1 lane 0 : tcgen05.mma issuer (leader CTA only)
-//   warp 2        : TMEM allocator (2 accumulators of BN_MAX columns: the epilogue of
-//                   tile i overlaps the mainloop of tile i+1)
+//   warp 2        : TMEM allocator (2 accumulator slots of min(BN_MAX, 256) columns: the
+//                   epilogue of tile i overlaps the mainloop of tile i+1; BN_MAX = 512 pair
+//                   tiles issue two N = 256 MMAs per k-step sharing the A tile and use both)
 //   warps 4..7    : epilogue (tcgen05.ld -> registers -> global, or -> swizzled smem ->
 //                   TMA store for EPI = 3), TMEM lanes 32*(w%4)..
 // Tiles: 128 rows per CTA, bn columns (runtime, <= BN_MAX), K atoms of 64 (one 128-byte
@@ -112,7 +113,9 @@ struct TileCfg {
   static constexpr uint32_t B_BYTES = KS * B_ATOM;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   // EPI = 3: per epilogue warp kStgBufs 32-row x 64-column bf16 staging tiles (128B swizzle)
-  static constexpr uint32_t STG_BYTES = EPI == 3 ? 4 * kStgBufs * 4096 : 0;
+  // (2 for 512-wide tiles, whose 4 ring stages of 48 KB leave 32 KB)
+  static constexpr int STG_BUFS = BN_MAX > 256 ? 2 : kStgBufs;
+  static constexpr uint32_t STG_BYTES = EPI == 3 ? 4 * STG_BUFS * 4096 : 0;
   // up to ~225 KB of the 227 KB opt-in smem per SM (7 stages for the 256x256 pair tiles)
   static constexpr int STAGES_RAW = ((OCC == 1 ? 225 : 110) * 1024 - STG_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
@@ -148,6 +151,20 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& g, int u) {
   t.m_blk = m_first + r % g_rows;
   t.n_blk = r / g_rows;
   return t;
+}
+
+// The i-th unit of CTA group `group` (static round-robin: units group, group + ngroups, ..),
+// -1 past its last.  (Walking odd groups' units in reverse, to stagger the wide tiles'
+// exposed epilogues, measured 12 µs slower at C2: it breaks the raster's L2 locality.)
+__device__ __forceinline__ int unit_of(const GemmArgs& g, int group, int ngroups, int i) {
+  const int u = group + i * ngroups;
+  return u < g.total_units ? u : -1;
+}
+
+// MMAs of N = slot_w per k-step for a unit: 2 for a 512-wide tile unless its second half lies
+// wholly past N (the ragged last column tile runs as one MMA, one B box, one TMEM slot).
+__device__ __forceinline__ int unit_halves(const Prob& p, int n_blk, int slot_w) {
+  return (p.bn > slot_w && n_blk * p.bn + slot_w < p.N) ? 2 : 1;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
@@ -208,6 +225,38 @@ __device__ __forceinline__ void store_row_segment(const Prob& p, int split, int 
 }
 
 
+// EPI = 3: one 32-row x 64-column bf16 chunk of a warp (row = lane) -> its staging buffer
+// (128B swizzle: 16-byte chunk e of row r at (e ^ (r & 7)) * 16) -> TMA store.  A buffer is
+// reused only after the store issued NB chunks earlier has finished reading it.
+template <int NB>
+__device__ __forceinline__ void stage_store_chunk(const uint32_t (&v)[2][32], uint8_t* stg, int& st_it, int lane,
+                                                  const CUtensorMap* dmap, int col, int row0) {
+  const int buf = st_it % NB;
+  if (st_it >= NB) {
+    if (lane == 0) bulk_wait_read<NB - 1>();
+    __syncwarp();
+  }
+  uint8_t* rowp = stg + buf * 4096 + lane * 128;
+  const uint32_t sw = (uint32_t)lane & 7u;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const uint32_t* x = &v[e >> 2][8 * (e & 3)];
+    uint4 o;
+    o.x = pack_bf16x2(__uint_as_float(x[0]), __uint_as_float(x[1]));
+    o.y = pack_bf16x2(__uint_as_float(x[2]), __uint_as_float(x[3]));
+    o.z = pack_bf16x2(__uint_as_float(x[4]), __uint_as_float(x[5]));
+    o.w = pack_bf16x2(__uint_as_float(x[6]), __uint_as_float(x[7]));
+    *reinterpret_cast<uint4*>(rowp + ((e ^ sw) << 4)) = o;
+  }
+  fence_proxy_async_shared();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(dmap, stg + buf * 4096, col, row0);
+    bulk_commit();
+  }
+  ++st_it;
+}
+
 // EPI = 0: epilogue stores from registers; EPI = 3: TMA-store epilogue (plain bf16 outputs).
 // KS: 64-wide K atoms per pipeline stage (TileCfg).
 template <int BN_MAX, int CG, int OCC = 1, int EPI = 0, int KS = 1>
@@ -217,7 +266,12 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
   // runtime ring depth <= the compiled maximum (fewer stages leave shared memory to kernels
   // that should co-reside, e.g. NCCL's during an overlapped allreduce)
   const int STAGES = (g.stages > 0 && g.stages < C::STAGES) ? g.stages : C::STAGES;
-  static_assert(BN_MAX % (16 * CG) == 0 && BN_MAX >= 16 && BN_MAX <= 256, "UMMA N");
+  static_assert(BN_MAX % (16 * CG) == 0 && BN_MAX >= 16 && (BN_MAX <= 256 || (BN_MAX == 512 && CG == 2)), "UMMA N");
+  // TMEM: two accumulator slots of SLOT_W columns.  A unit of bn <= SLOT_W uses one slot (the
+  // epilogue of unit i overlaps the mainloop of unit i+1); a 512-wide pair tile (BN_MAX = 512:
+  // two N = 256 MMAs per k-step sharing the A tile) uses both.
+  constexpr int SLOT_W = BN_MAX <= 256 ? BN_MAX : 256;
+  constexpr uint32_t kBHalf = (SLOT_W / CG) * 128;  // K-major B bytes of one MMA's columns per CTA
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -273,8 +327,8 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
     int stage = 0;
     uint32_t phase = 0;
     for (int i_u = 0;; ++i_u) {
-      const int u = group + i_u * ngroups;
-      if (u >= g.total_units) break;
+      const int u = unit_of(g, group, ngroups, i_u);
+      if (u < 0) break;
       const Unit t = decode_unit(g, u);
       const Prob& p = g.p[t.prob];
       if (g.trace && lane == 0) {
@@ -285,6 +339,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       const int m0 = t.m_blk * (kBM * CG) + rank * kBM;
       const int nb = p.bn / CG;  // B columns held by this CTA
       const int n0 = t.n_blk * p.bn + rank * nb;
+      const int nh = BN_MAX > SLOT_W ? unit_halves(p, t.n_blk, SLOT_W) : 1;
       const int kb0 = t.split * p.kb_per_split;
       const int kb1 = min(p.nk1, kb0 + p.kb_per_split);
       const int nmain = kb1 - kb0;
@@ -301,8 +356,10 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
           const int natoms = min(KS, nkb - i0);
           uint64_t* fb = &full[stage];
           const bool skip_a = g.dbg == 6 || (g.dbg == 7 && (i0 & 1));
+          // a ragged 512-wide tile loads one B box per CTA
+          const uint32_t full_tx = (BN_MAX > SLOT_W && p.bn > SLOT_W && nh == 1) ? p.stage_tx - CG * kBHalf : p.stage_tx;
           const uint32_t tx = g.dbg == 5 ? (uint32_t)(CG * kBM * kBK * 2)
-                              : skip_a ? p.stage_tx - (uint32_t)(CG * kBM * kBK * 2) : p.stage_tx;
+                              : skip_a ? full_tx - (uint32_t)(CG * kBM * kBK * 2) : full_tx;
           if (leader) mbar_arrive_expect_tx(fb, tx * (uint32_t)natoms);
           for (int at = 0; at < natoms; ++at) {
             const int i = i0 + at;
@@ -327,7 +384,14 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
             }
             if (g.dbg == 5) {
             } else if (!p.b_mn) {
-              tma_load_2d<CG>(tb, fb, b, kcb, n0, p.hint_b);
+              if (BN_MAX > SLOT_W && p.bn > SLOT_W) {
+                // two MMAs of N = SLOT_W: this CTA holds columns [SLOT_W*h + rank*SLOT_W/CG, +SLOT_W/CG) of MMA h
+                const int tn = t.n_blk * p.bn + (int)rank * (SLOT_W / CG);
+                tma_load_2d<CG>(tb, fb, b, kcb, tn, p.hint_b);
+                if (nh == 2) tma_load_2d<CG>(tb, fb, b + kBHalf, kcb, tn + SLOT_W, p.hint_b);
+              } else {
+                tma_load_2d<CG>(tb, fb, b, kcb, n0, p.hint_b);
+              }
             } else if (p.b_3d) {
               tma_load_3d<CG>(tb, fb, b, 0, kcb, n0 / cw, p.hint_b);
             } else {
@@ -349,9 +413,11 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
     // lane issues tcgen05.mma / tcgen05.commit.
     int stage = 0;
     uint32_t phase = 0;
+    int sc = 0;                  // accumulator slots handed out so far (slot = sc & 1)
+    uint32_t use0 = 0, use1 = 0;  // uses of slot 0 / 1 (mbarrier phase parity)
     for (int it = 0;; ++it) {
-      const int u = group + it * ngroups;
-      if (u >= g.total_units) break;
+      const int u = unit_of(g, group, ngroups, it);
+      if (u < 0) break;
       const Unit t = decode_unit(g, u);
       const Prob& p = g.p[t.prob];
       const int kb0 = t.split * p.kb_per_split;
@@ -361,11 +427,15 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       // snake: every other round of this CTA walks K backwards, starting where the data it
       // (and its neighbours) just streamed is still in L2
       const bool rev = p.snake && (it & 1);
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      const int nh = BN_MAX > SLOT_W ? unit_halves(p, t.n_blk, SLOT_W) : 1;
+      const int s0 = sc & 1;
+      for (int h = 0; h < nh; ++h) {
+        const int sl = s0 ^ h;
+        mbar_wait(&tempty[sl], ((sl ? use1 : use0) & 1) ^ 1);
+      }
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN_MAX;
+      const uint32_t d_tmem = tmem_base + (uint32_t)(s0 * SLOT_W);
+      const uint32_t d_tmem1 = tmem_base + (uint32_t)((s0 ^ 1) * SLOT_W);
       const uint32_t a_step = p.a_mn ? 2048u : 32u;
       const uint32_t b_swz = p.b_mn ? (uint32_t)p.b_swz : 128u;
       const uint32_t b_step = p.b_mn ? 16u * b_swz : 32u;
@@ -387,6 +457,10 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
               const uint64_t ad = a_hi | (uint64_t)(((a_addr + j * a_step) >> 4) & 0x3FFF);
               const uint64_t bd = b_hi | (uint64_t)(((b_addr + j * b_step) >> 4) & 0x3FFF);
               umma_f16<CG>(d_tmem, ad, bd, p.idesc, (i > 0 || j > 0) ? 1u : 0u);
+              if (BN_MAX > SLOT_W && nh == 2) {
+                const uint64_t bd1 = b_hi | (uint64_t)(((b_addr + kBHalf + j * b_step) >> 4) & 0x3FFF);
+                umma_f16<CG>(d_tmem1, ad, bd1, p.idesc, (i > 0 || j > 0) ? 1u : 0u);
+              }
             }
           }
           umma_commit<CG>(&empty[stage]);  // frees the smem slot(s) when these MMAs retire
@@ -397,127 +471,146 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
           phase ^= 1;
         }
       }
-      if (elect_one_sync()) umma_commit<CG>(&tfull[acc]);  // accumulator ready for the epilogue(s)
+      if (elect_one_sync()) {  // accumulator(s) ready for the epilogue(s)
+        umma_commit<CG>(&tfull[s0]);
+        if (nh == 2) umma_commit<CG>(&tfull[s0 ^ 1]);
+      }
       __syncwarp();
+      for (int h = 0; h < nh; ++h) {
+        if (s0 ^ h) ++use1;
+        else ++use0;
+      }
+      sc += nh;
     }
   } else if (warp >= 4) {
     // --------------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int it = 0;
     int st_it = 0;  // EPI = 3: TMA stores issued by this warp
+    int sc = 0;     // accumulator slots consumed (same sequence as the MMA issuer)
+    uint32_t use0 = 0, use1 = 0;
     for (;; ++it) {
-      const int u = group + it * ngroups;
-      if (u >= g.total_units) break;
+      const int u = unit_of(g, group, ngroups, it);
+      if (u < 0) break;
       const Unit t = decode_unit(g, u);
       const Prob& p = g.p[t.prob];
       const int m0 = t.m_blk * (kBM * CG) + rank * kBM;
       const int n0 = t.n_blk * p.bn;
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
       const int row = (g.dbg == 3) ? 0x7fffffff : m0 + q * 32 + lane;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN_MAX;
-      if (g.dbg == 4) {
-      } else if (EPI == 3) {
-        // bf16 tile -> per-warp swizzled smem staging -> TMA store (coalesced full-line
-        // writes; rows >= M / cols >= N are clipped by the tensor map bounds).  64-column
-        // chunks, kStgBufs staging tiles per warp: a buffer is reused only after the store
-        // issued kStgBufs chunks earlier has finished reading it.
-        uint8_t* stg = smem + STAGES * C::STAGE_BYTES + q * (kStgBufs * 4096);
-        const uint32_t sw = (uint32_t)lane & 7u;  // 128B swizzle: 16B chunk ^= row bits [0,3)
-#pragma unroll 1
-        for (int c = 0; c < p.bn; c += 64) {
-          if (n0 + c >= p.N) break;  // warp-uniform
-          const int buf = st_it % kStgBufs;
-          if (st_it >= kStgBufs) {
-            if (lane == 0) bulk_wait_read<kStgBufs - 1>();
-            __syncwarp();
-          }
-          uint8_t* rowp = stg + buf * 4096 + lane * 128;
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(t_row + c + 32 * hf, v);
+      const int nh = BN_MAX > SLOT_W ? unit_halves(p, t.n_blk, SLOT_W) : 1;
+      for (int h = 0; h < nh; ++h) {  // slot by slot: the first is released while the second drains
+        const int sl = (sc & 1) ^ h;
+        mbar_wait(&tfull[sl], (sl ? use1 : use0) & 1);
+        tc_fence_after();
+        const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + (uint32_t)(sl * SLOT_W);
+        const int bw = min(p.bn - h * SLOT_W, SLOT_W);  // columns of this slot
+        const int nc = n0 + h * SLOT_W;                 // their first output column
+        if (g.dbg == 4) {
+        } else if (EPI == 3) {
+          // bf16 tile -> per-warp swizzled smem staging -> TMA store (coalesced full-line
+          // writes; rows >= M / cols >= N are clipped by the tensor map bounds).  64-column
+          // chunks, STG_BUFS staging tiles per warp: a buffer is reused only after the store
+          // issued STG_BUFS chunks earlier has finished reading it.
+          uint8_t* stg = smem + STAGES * C::STAGE_BYTES + q * (C::STG_BUFS * 4096);
+          // software pipelined: the TMEM loads of chunk i+1 are in flight while chunk i is
+          // packed, staged and stored
+          const int nch = min(bw, p.N - nc + 63) / 64;  // 64-column chunks inside N
+          const CUtensorMap* dmap = &tm.m[t.prob][4];
+          uint32_t va[2][32], vb[2][32];
+          if (nch > 0) {
+            tmem_ld_32x32b_x32(t_row, va[0]);
+            tmem_ld_32x32b_x32(t_row + 32, va[1]);
             tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              uint4 o;
-              o.x = pack_bf16x2(__uint_as_float(v[8 * e + 0]), __uint_as_float(v[8 * e + 1]));
-              o.y = pack_bf16x2(__uint_as_float(v[8 * e + 2]), __uint_as_float(v[8 * e + 3]));
-              o.z = pack_bf16x2(__uint_as_float(v[8 * e + 4]), __uint_as_float(v[8 * e + 5]));
-              o.w = pack_bf16x2(__uint_as_float(v[8 * e + 6]), __uint_as_float(v[8 * e + 7]));
-              *reinterpret_cast<uint4*>(rowp + (((4 * hf + e) ^ sw) << 4)) = o;
+            reg_fence32(va[0]);
+            reg_fence32(va[1]);
+          }
+#pragma unroll 1
+          for (int i = 0; i < nch; i += 2) {
+            if (i + 1 < nch) {
+              tmem_ld_32x32b_x32(t_row + 64 * (i + 1), vb[0]);
+              tmem_ld_32x32b_x32(t_row + 64 * (i + 1) + 32, vb[1]);
+            }
+            stage_store_chunk<C::STG_BUFS>(va, stg, st_it, lane, dmap, nc + 64 * i, m0 + q * 32);
+            if (i + 1 < nch) {
+              tmem_ld_wait();
+              reg_fence32(vb[0]);
+              reg_fence32(vb[1]);
+              if (i + 2 < nch) {
+                tmem_ld_32x32b_x32(t_row + 64 * (i + 2), va[0]);
+                tmem_ld_32x32b_x32(t_row + 64 * (i + 2) + 32, va[1]);
+              }
+              stage_store_chunk<C::STG_BUFS>(vb, stg, st_it, lane, dmap, nc + 64 * (i + 1), m0 + q * 32);
+              if (i + 2 < nch) {
+                tmem_ld_wait();
+                reg_fence32(va[0]);
+                reg_fence32(va[1]);
+              }
             }
           }
-          fence_proxy_async_shared();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&tm.m[t.prob][4], stg + buf * 4096, n0 + c, m0 + q * 32);
-            bulk_commit();
-          }
-          ++st_it;
-        }
-      } else if (p.out_mode == OUT_F32_FOLD) {
-        // sum of the fold column blocks (w = fold_w in {8, 16, 32}), in block order
-        float o[32];
+        } else if (p.out_mode == OUT_F32_FOLD) {
+          // sum of the fold column blocks (w = fold_w in {8, 16, 32}), in block order
+          float o[32];
 #pragma unroll
-        for (int x = 0; x < 32; ++x) o[x] = 0.f;
-        const int w = p.fold_w;
+          for (int x = 0; x < 32; ++x) o[x] = 0.f;
+          const int w = p.fold_w;
 #pragma unroll 1
-        for (int c = 0; c < p.bn; c += 32) {
-          uint32_t v[32];
-          const bool full32 = p.bn - c >= 32;
-          if (full32) tmem_ld_32x32b_x32(t_row + c, v);
-          else tmem_ld_32x32b_x16(t_row + c, v);
-          tmem_ld_wait();
-          if (w == 32) {
+          for (int c = 0; c < bw; c += 32) {
+            uint32_t v[32];
+            const bool full32 = bw - c >= 32;
+            if (full32) tmem_ld_32x32b_x32(t_row + c, v);
+            else tmem_ld_32x32b_x16(t_row + c, v);
+            tmem_ld_wait();
+            if (w == 32) {
 #pragma unroll
-            for (int x = 0; x < 32; ++x) o[x] += __uint_as_float(v[x]);
-          } else if (w == 16) {
+              for (int x = 0; x < 32; ++x) o[x] += __uint_as_float(v[x]);
+            } else if (w == 16) {
 #pragma unroll
-            for (int x = 0; x < 16; ++x) o[x] += __uint_as_float(v[x]);
-            if (full32) {
+              for (int x = 0; x < 16; ++x) o[x] += __uint_as_float(v[x]);
+              if (full32) {
 #pragma unroll
-              for (int x = 0; x < 16; ++x) o[x] += __uint_as_float(v[16 + x]);
-            }
-          } else {
+                for (int x = 0; x < 16; ++x) o[x] += __uint_as_float(v[16 + x]);
+              }
+            } else {
 #pragma unroll
-            for (int b8 = 0; b8 < 4; ++b8) {
-              if (b8 >= 2 && !full32) break;
+              for (int b8 = 0; b8 < 4; ++b8) {
+                if (b8 >= 2 && !full32) break;
 #pragma unroll
-              for (int x = 0; x < 8; ++x) o[x] += __uint_as_float(v[8 * b8 + x]);
+                for (int x = 0; x < 8; ++x) o[x] += __uint_as_float(v[8 * b8 + x]);
+              }
             }
           }
-        }
-        if (row < p.M) {
-          float* dst = static_cast<float*>(p.D) + t.split * p.split_stride + (long long)row * p.ldd;
+          if (row < p.M) {
+            float* dst = static_cast<float*>(p.D) + t.split * p.split_stride + (long long)row * p.ldd;
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            if (4 * e < w) *reinterpret_cast<float4*>(dst + 4 * e) = make_float4(o[4 * e], o[4 * e + 1], o[4 * e + 2], o[4 * e + 3]);
-        }
-      } else if (p.bn % 32 == 0) {
+            for (int e = 0; e < 8; ++e)
+              if (4 * e < w) *reinterpret_cast<float4*>(dst + 4 * e) = make_float4(o[4 * e], o[4 * e + 1], o[4 * e + 2], o[4 * e + 3]);
+          }
+        } else if (bw % 32 == 0) {
 #pragma unroll 1
-        for (int c = 0; c < p.bn; c += 32) {
-          if (n0 + c >= p.N) break;  // warp-uniform
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(t_row + c, v);
-          tmem_ld_wait();
-          if (row < p.M) store_row_segment(p, t.split, row, n0 + c, v, 32);
-        }
-      } else {
+          for (int c = 0; c < bw; c += 32) {
+            if (nc + c >= p.N) break;  // warp-uniform
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(t_row + c, v);
+            tmem_ld_wait();
+            if (row < p.M) store_row_segment(p, t.split, row, nc + c, v, 32);
+          }
+        } else {
 #pragma unroll 1
-        for (int c = 0; c < p.bn; c += 16) {
-          if (n0 + c >= p.N) break;
-          uint32_t v[32];
-          tmem_ld_32x32b_x16(t_row + c, v);
-          tmem_ld_wait();
-          if (row < p.M) store_row_segment(p, t.split, row, n0 + c, v, 16);
+          for (int c = 0; c < bw; c += 16) {
+            if (nc + c >= p.N) break;
+            uint32_t v[32];
+            tmem_ld_32x32b_x16(t_row + c, v);
+            tmem_ld_wait();
+            if (row < p.M) store_row_segment(p, t.split, row, nc + c, v, 16);
+          }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote<CG>(&tempty[sl], 0);  // leader's barrier
+        if (sl) ++use1;
+        else ++use0;
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote<CG>(&tempty[acc], 0);  // leader's barrier
+      sc += nh;
       if (g.trace && threadIdx.x == 4 * 32) g.trace[8 * u + 3] = globaltimer();
     }
     if constexpr (EPI == 3) {

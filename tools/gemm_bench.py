@@ -54,6 +54,7 @@ def main():
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--splits", type=int, default=1)
     ap.add_argument("--cublas", action="store_true")
+    ap.add_argument("--check", action="store_true", help="compare D with an fp32 torch product (K2 = 0, K-major)")
     ap.add_argument("--sustain", type=float, default=0.0, help="also run back-to-back for this many seconds, "
                     "sampling SM clock and power")
     a = ap.parse_args()
@@ -92,6 +93,11 @@ def main():
             ts.append(e0.elapsed_time(e1))
         ts.sort()
         med = ts[len(ts) // 2]
+        if a.check:
+            ref = A.float() @ B.float().t()
+            err = ((D.float() - ref).norm() / ref.norm()).item()
+            print(json.dumps({"check": "tc_gemm", "cg": cg, "bn": a.bn, "rel_fro": err}), flush=True)
+            assert err < 1e-2, err
         rec = {"kernel": "tc_gemm", "cg": cg, "bn": a.bn, "M": M, "N": N, "K": K, "K2": a.K2, "splits": a.splits,
                "GBps_A": (M * K * 2) / (med * 1e-3) / 1e9,
                "a_mn": a.a_mn, "b_mn": a.b_mn, "median_us": med * 1e3, "min_us": ts[0] * 1e3,
