@@ -29,8 +29,8 @@ Ctx::Ctx(int device) : device_(device) {
   if (const char* e = getenv("RUNLORA_TMA_STORE_MAIN")) tma_store_main_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_MAIN_WIDE")) main_wide_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_WIDE_COST")) {
-    double b = 0, sm = 0;
-    if (sscanf(e, "%lf,%lf", &b, &sm) == 2 && b > 0 && sm > 0) wide_cost_big_ = b, wide_cost_small_ = sm;
+    double a = 0, k = 0;
+    if (sscanf(e, "%lf,%lf", &a, &k) == 2 && a > 0 && k >= 0) wide_cost_a_ = a, wide_cost_e_ = k;
   }
   if (const char* e = getenv("RUNLORA_TMA_STORE_WPRIME")) tma_store_wprime_ = atoi(e) != 0;
   int prev = -1;

@@ -96,11 +96,12 @@ class Ctx {
   int trace_kid = -1;
   static constexpr int kTraceUnits = 1 << 16;  // == kTraceMaxUnits (tc_gemm.cuh); + 4 words per CTA
   bool tma_store_main() const { return tma_store_main_; }
-  // 512-wide pair tiles for the main GEMMs (env RUNLORA_MAIN_WIDE=0 disables); unit costs of
-  // the planner (env RUNLORA_WIDE_COST="big,small", in MMA-only 256x256 tile times)
+  // 512-wide pair tiles for the main GEMMs (env RUNLORA_MAIN_WIDE=0 disables).  Planner cost
+  // of a 512-wide tile in 256-wide tile times: a + e / K (env RUNLORA_WIDE_COST="a,e").
   bool main_wide() const { return main_wide_; }
-  double wide_cost_big() const { return wide_cost_big_; }
-  double wide_cost_small() const { return wide_cost_small_; }
+  double wide_cost_a() const { return wide_cost_a_; }
+  double wide_cost_e() const { return wide_cost_e_; }
+  std::map<std::tuple<int, int, int, int>, int>& wide_cache() { return wide_cache_; }
   // main-GEMM pipeline stages (env RUNLORA_MAIN_STAGES; 0 = all that fit = 7).  6 stages
   // cost ~1 % in a step (the GEMM alone: 166.9 µs either way; 5: 169, 4: 181) and leave
   // 32 KB of shared memory per SM, so NCCL's kernels can co-reside with the dX GEMM that
@@ -139,7 +140,8 @@ class Ctx {
   void* identity_ = nullptr;
   bool tma_store_main_ = false;   // env RUNLORA_TMA_STORE_MAIN=1
   bool main_wide_ = true;
-  double wide_cost_big_ = 2.2, wide_cost_small_ = 1.33;
+  double wide_cost_a_ = 1.69, wide_cost_e_ = 579.0;
+  std::map<std::tuple<int, int, int, int>, int> wide_cache_;  // (M, N, K, raster) -> rows_big
   int main_stages_ = 0;
   bool tma_store_wprime_ = true;  // env RUNLORA_TMA_STORE_WPRIME=0
   bool occ2_ = true;

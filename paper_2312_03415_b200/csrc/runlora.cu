@@ -524,13 +524,15 @@ runlora_status_t wprime_t_bf16(Ctx& c, const runlora_shape_t& s, const void* W, 
 
 // ------------------------------------------------------------ 512-wide main-GEMM tiles
 // A 256x512 pair tile (two N = 256 MMAs per k-step sharing the A tile) moves 25 % fewer TMA
-// bytes per FLOP than a 256x256 one; the main GEMM's time tracks those bytes,
-// but the tile's 512 accumulator columns leave no second TMEM buffer, so its epilogue is
-// exposed, and big tiles quantise badly on 74 pairs (C2: 256 tiles = 3.46 rounds).  So the
-// output rows [0, rows_big) run as 512-wide tiles and the rest as 256-wide ones in the same
-// launch (two problems); rows_big minimises the busiest pair's summed unit cost under the
-// kernel's static round-robin assignment (unit u -> pair u mod 74), costs in units of an
-// MMA-only 256x256 tile (measured: big 2.2 incl. the exposed epilogue, small 1.33).
+// bytes per FLOP than a 256x256 one, and the main GEMM's time tracks those bytes (DESIGN.md
+// §5); but its 512 accumulator columns leave no second TMEM buffer, so its epilogue (one
+// burst of output writes per round) is exposed, and big tiles quantise coarsely on 74 pairs
+// (C2: 256 tiles = 3.46 rounds).  So output rows [0, rows_big) run as 512-wide tiles and
+// the rest as 256-wide ones in the same launch (two problems).  rows_big minimises the
+// busiest pair's summed unit cost under the kernel's static round-robin assignment (unit u
+// -> pair u mod 74).  Cost of a 512-wide tile in 256-wide tile times: a + e / K, fitted to
+// gemm_bench runs at K = 2048 / 4096 / 11008 (1.95 / 1.83 / 1.74: a = 1.69, e = 579 — the
+// exposed epilogue, ~3.7 µs, against a 256-wide tile's ~6.3 ns per K).  Cached per shape.
 struct WideSplit {
   int rows_big;  // multiple of 256; 0 = no 512-wide tiles
   double cost, cost_small_only;
@@ -546,14 +548,22 @@ static void host_unit_tile(int u, int mt, int nt, int G, int* m_blk, int* n_blk)
   *n_blk = r / g_rows;
 }
 
-WideSplit wide_split(const Ctx& c, const GemmReq& q) {
+WideSplit wide_split(Ctx& c, const GemmReq& q) {
   WideSplit w{0, 0, 0};
+  if (!c.main_wide() || q.cg != 2 || q.a_mn || q.b_mn || q.splits > 1 || q.out_mode != OUT_BF16) return w;
+  const int G = raster_rows(q);
+  const int K = q.K1 + q.K2;
+  const auto key = std::make_tuple(q.M, q.N, K, G);
+  auto& cache = c.wide_cache();
+  if (auto it = cache.find(key); it != cache.end()) {
+    w.rows_big = it->second;
+    return w;
+  }
   const int pairs = c.num_sms() / 2;
   const int mt = (q.M + 255) / 256;
   const int ntb = (q.N + 511) / 512, nts = (q.N + 255) / 256;
   const bool ragged = (int64_t)ntb * 512 - q.N >= 256;  // last 512-wide column tile has one half
-  const double cb = c.wide_cost_big(), cs = c.wide_cost_small();
-  const int G = raster_rows(q);
+  const double cb = c.wide_cost_a() + c.wide_cost_e() / K, cs = 1.0;
   std::vector<double> load(pairs);
   auto simulate = [&](int rb) {
     std::fill(load.begin(), load.end(), 0.0);
@@ -568,11 +578,13 @@ WideSplit wide_split(const Ctx& c, const GemmReq& q) {
   };
   w.cost_small_only = simulate(0);
   w.cost = w.cost_small_only;
-  if (!c.main_wide() || q.cg != 2 || q.a_mn || q.b_mn || q.splits > 1 || q.out_mode != OUT_BF16) return w;
-  for (int rb = 1; rb <= mt; ++rb) {
+  // the 256-wide remainder only ever needs to fill the last round or two
+  const int lo = std::max(1, mt - (3 * pairs + nts - 1) / nts);
+  for (int rb = mt; rb >= lo; --rb) {
     const double t = simulate(rb);
     if (t < w.cost * 0.995) w.cost = t, w.rows_big = rb * 256;
   }
+  cache[key] = w.rows_big;
   return w;
 }
 
