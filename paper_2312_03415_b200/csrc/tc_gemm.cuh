@@ -277,7 +277,8 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+  // [A ring | B ring | EPI = 3 staging | barriers]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES + C::STG_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
