@@ -37,6 +37,11 @@ int runlora_debug_trace(runlora_handle_t h, unsigned long long* host, int max_un
  * synchronises the device.  Returns the number of launches copied. */
 int runlora_debug_ltrace(runlora_handle_t h, unsigned long long* host, int* kids, int max_launches);
 const char* runlora_debug_kernel_name(int kid);
+/* The main-GEMM tile split (DESIGN.md §5 "512-wide main-GEMM tiles"): for an M x N bf16
+ * output with reduction length K and a K-major B operand (b_mn = 0), the number of leading
+ * output rows the library runs as 256x512 pair tiles (a multiple of 256; 0 = 256-wide tiles
+ * only, also when b_mn != 0 or env RUNLORA_MAIN_WIDE=0).  Host-only; -1 on a bad handle. */
+int runlora_debug_wide_rows(runlora_handle_t h, int M, int N, int K, int b_mn);
 #ifdef __cplusplus
 }
 #endif

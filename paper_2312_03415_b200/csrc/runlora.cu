@@ -1431,6 +1431,15 @@ extern "C" int runlora_debug_ltrace(runlora_handle_t h, unsigned long long* host
   return h->ctx->ltrace_read(host, kids, max_launches);
 }
 
+extern "C" int runlora_debug_wide_rows(runlora_handle_t h, int M, int N, int K, int b_mn) {
+  if (!h || !h->ctx || M <= 0 || N <= 0 || K <= 0) return -1;
+  GemmReq q = main_req(*h->ctx, M, N);
+  q.K1 = K;
+  q.b_mn = b_mn != 0;
+  if (main_split(M, N, K).splits > 1) return 0;  // small-M split-K path (main_gemm)
+  return wide_split(*h->ctx, q).rows_big;
+}
+
 extern "C" const char* runlora_debug_kernel_name(int kid) {
   return (kid >= 0 && kid < KID_COUNT) ? kKernelNames[kid] : "?";
 }

@@ -1,0 +1,79 @@
+"""512-wide main-GEMM tiles: the planner's split and parity of every
+executable variant on shapes where it mixes 512- and 256-wide tiles, with ragged rows,
+a ragged last column tile of one MMA half (N = 3304: 232 columns) and of two halves
+(N = 3512: 440 columns), and the concat-K tail of dX — against the fp64 oracle
+(relative Frobenius <= 2e-2 per tensor, healthy < 5e-3)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rl():
+    from paper_2312_03415_b200 import runlora
+    return runlora
+
+
+def _rows(rl, h, M, N, K, b_mn=0):
+    f = rl._lib.runlora_debug_wide_rows
+    f.restype = C.c_int
+    f.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
+    return f(h._h, M, N, K, b_mn)
+
+
+def _np(t):
+    return t.detach().to(torch.float64).cpu().numpy()
+
+
+def test_planner_split(rl):
+    h = rl.handle(0)
+    # Y GEMM of case W1 (M = n, N = m, K = k): wide rows then narrow rows (ragged M)
+    r = _rows(rl, h, 3000, 3304, 2048)
+    assert 0 < r < 3000 and r % 256 == 0
+    # C2: most rows wide (measured planner choice 6912 of 8192)
+    r = _rows(rl, h, 8192, 4096, 4096)
+    assert 4096 <= r < 8192 and r % 256 == 0
+    # MN-major B (forward1's Y GEMM) and single-round shapes stay 256-wide
+    assert _rows(rl, h, 8192, 4096, 4096, b_mn=1) == 0
+    assert _rows(rl, h, 512, 512, 512) == 0
+    # short K: the exposed epilogue outweighs the traffic saving
+    assert _rows(rl, h, 4096, 3000, 776) == 0
+
+
+CASES = [synth.case("wide_w1", 0, 40, 3000, 2048, 3304, 16, "bf16"),
+         synth.case("wide_w2", 0, 41, 2600, 3512, 2048, 8, "bf16")]
+
+
+@pytest.mark.parametrize("c", CASES, ids=lambda c: c.name)
+def test_wide_all_variants_match_oracle(rl, c):
+    h = rl.handle(0)
+    # both main GEMMs of the case take the wide path
+    assert _rows(rl, h, c.n, c.m, c.k) > 0 and _rows(rl, h, c.n, c.k, c.m + c.r) > 0
+    ops = synth.operands(c)
+    d = {k: v.cuda() for k, v in ops.items()}
+    shape = rl.make_shape(c.n, c.k, c.m, c.r, rl.BF16)
+    X, W, A, B, dY = (_np(ops[k]) for k in ("X", "W", "A", "B", "dY"))
+    wY = O.forward(1, X, W, A, B)
+    wA, wB, wX = O.reference_backward(X, W, A, B, dY)
+    errs = {}
+    for f in (1, 2):
+        Y = torch.full((c.n, c.m), float("nan"), dtype=torch.bfloat16, device="cuda")
+        h.forward(f, shape, d["X"], d["W"], d["A"], d["B"], Y)
+        torch.cuda.synchronize()
+        errs[f"F{f}"] = O.rel_fro(_np(Y), wY)
+    for b in (1, 2, 3, 4, 5):
+        dX = torch.full((c.n, c.k), float("nan"), dtype=torch.bfloat16, device="cuda")
+        dA = torch.full((c.k, c.r), float("nan"), device="cuda")
+        dB = torch.full((c.r, c.m), float("nan"), device="cuda")
+        h.backward(b, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], dX, dA, dB)
+        torch.cuda.synchronize()
+        errs[f"B{b}"] = max(O.rel_fro(_np(dA), wA), O.rel_fro(_np(dB), wB), O.rel_fro(_np(dX), wX))
+    assert all(e <= 2e-2 for e in errs.values()), errs
+    assert max(errs.values()) < 5e-3, errs
