@@ -430,10 +430,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       const bool rev = p.snake && (it & 1);
       const int nh = BN_MAX > SLOT_W ? unit_halves(p, t.n_blk, SLOT_W) : 1;
       const int s0 = sc & 1;
-      for (int h = 0; h < nh; ++h) {
-        const int sl = s0 ^ h;
-        mbar_wait(&tempty[sl], ((sl ? use1 : use0) & 1) ^ 1);
-      }
+      mbar_wait(&tempty[s0], ((s0 ? use1 : use0) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(s0 * SLOT_W);
       const uint32_t d_tmem1 = tmem_base + (uint32_t)((s0 ^ 1) * SLOT_W);
@@ -442,28 +439,67 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       const uint32_t b_step = p.b_mn ? 16u * b_swz : 32u;
       const uint64_t a_hi = smem_desc(0, p.a_mn ? 8192 : 16, 1024, 2u);
       const uint64_t b_hi = smem_desc(0, p.b_mn ? 64u * b_swz : 16u, 8u * b_swz, sw_layout_code(b_swz));
-      for (int i0 = 0; i0 < nkb; i0 += KS) {
-        if (g.dbg != 1 && g.dbg != 3 && g.dbg != 4) mbar_wait(&full[stage], phase);
-        tc_fence_after();
+      // MMAs of k-block group i0 from ring slot st for the halves in hmask (bit h: MMA h)
+      auto issue = [&](int st, int i0, int hmask) {
         const int natoms = min(KS, nkb - i0);
-        if (elect_one_sync()) {
-          for (int at = 0; at < natoms; ++at) {
-            const int i = i0 + at;
-            const int ki = rev ? nmain - 1 - i : i;
-            const int kleft = (i < nmain) ? (p.k1 - (kb0 + ki) * kBK) : (p.k2 - (i - nmain) * kBK);
-            const int ksteps = min(kBK / 16, (kleft + 15) >> 4);
-            const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES + at * C::A_ATOM);
-            const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES + at * C::B_ATOM);
-            for (int j = 0; j < (g.dbg == 2 ? 0 : ksteps); ++j) {
-              const uint64_t ad = a_hi | (uint64_t)(((a_addr + j * a_step) >> 4) & 0x3FFF);
+        for (int at = 0; at < natoms; ++at) {
+          const int i = i0 + at;
+          const int ki = rev ? nmain - 1 - i : i;
+          const int kleft = (i < nmain) ? (p.k1 - (kb0 + ki) * kBK) : (p.k2 - (i - nmain) * kBK);
+          const int ksteps = min(kBK / 16, (kleft + 15) >> 4);
+          const uint32_t a_addr = smem_u32(sA + st * C::A_BYTES + at * C::A_ATOM);
+          const uint32_t b_addr = smem_u32(sB + st * C::B_BYTES + at * C::B_ATOM);
+          for (int j = 0; j < (g.dbg == 2 ? 0 : ksteps); ++j) {
+            const uint64_t ad = a_hi | (uint64_t)(((a_addr + j * a_step) >> 4) & 0x3FFF);
+            if (hmask & 1) {
               const uint64_t bd = b_hi | (uint64_t)(((b_addr + j * b_step) >> 4) & 0x3FFF);
               umma_f16<CG>(d_tmem, ad, bd, p.idesc, (i > 0 || j > 0) ? 1u : 0u);
-              if (BN_MAX > SLOT_W && nh == 2) {
-                const uint64_t bd1 = b_hi | (uint64_t)(((b_addr + kBHalf + j * b_step) >> 4) & 0x3FFF);
-                umma_f16<CG>(d_tmem1, ad, bd1, p.idesc, (i > 0 || j > 0) ? 1u : 0u);
-              }
+            }
+            if (BN_MAX > SLOT_W && (hmask & 2)) {
+              const uint64_t bd1 = b_hi | (uint64_t)(((b_addr + kBHalf + j * b_step) >> 4) & 0x3FFF);
+              umma_f16<CG>(d_tmem1, ad, bd1, p.idesc, (i > 0 || j > 0) ? 1u : 0u);
             }
           }
+        }
+      };
+      int i_start = 0;
+      if (BN_MAX > SLOT_W && nh == 2) {
+        // Second slot still draining (the previous wide tile's epilogue releases slot s0
+        // first): run MMA 0 alone on up to STAGES k-blocks, holding their ring slots, then
+        // catch MMA 1 up on them once its slot is free.
+        const uint32_t par1 = (((s0 ^ 1) ? use1 : use0) & 1) ^ 1;
+        const int st0 = stage;
+        int npre = 0;
+        while (npre < STAGES && npre * KS < nkb) {
+          const bool free1 = __shfl_sync(0xffffffffu, mbar_test(&tempty[s0 ^ 1], par1) ? 1 : 0, 0) != 0;
+          if (free1) break;
+          if (g.dbg != 1 && g.dbg != 3 && g.dbg != 4) mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one_sync()) issue(stage, npre * KS, 1);
+          __syncwarp();
+          ++npre;
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mbar_wait(&tempty[s0 ^ 1], par1);
+        tc_fence_after();
+        for (int q2 = 0; q2 < npre; ++q2) {
+          const int st = (st0 + q2) % STAGES;
+          if (elect_one_sync()) {
+            issue(st, q2 * KS, 2);
+            umma_commit<CG>(&empty[st]);
+          }
+          __syncwarp();
+        }
+        i_start = npre * KS;
+      }
+      for (int i0 = i_start; i0 < nkb; i0 += KS) {
+        if (g.dbg != 1 && g.dbg != 3 && g.dbg != 4) mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one_sync()) {
+          issue(stage, i0, nh == 2 ? 3 : 1);
           umma_commit<CG>(&empty[stage]);  // frees the smem slot(s) when these MMAs retire
         }
         __syncwarp();
