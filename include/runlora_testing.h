@@ -12,7 +12,8 @@
  *   A2/B2: same majors with K2 (K2 == 0: no tail)
  *   out_mode 0: D bf16 [M, N]; 1: D bf16 = acc + Cin (bf16 [M, N]);
  *            2: D fp32 partial slabs [splits][M][N] (split-K over K1)
- *   BN: tile width (16, 32, 48, 64, 128, 256; MN-major B: 16, 32 or a multiple of 64).
+ *   BN: tile width (16, 32, 48, 64, 128, 256, 512 with cg = 2 and K-major B; MN-major B: 16, 32 or a
+ *       multiple of 64); 0 = the main GEMMs' launch (cg = 2, bf16 output, 512/256-wide split by the planner).
  *   cg: 1 = one CTA per 128-row tile; 2 = CTA pair (tcgen05 cta_group::2) per 256-row tile.
  * All pointers are device pointers; rows are contiguous (ld = number of columns).
  */

@@ -592,37 +592,43 @@ static DeviceMat rows_from(const DeviceMat& m, int64_t r0) {
   return DeviceMat{static_cast<const char*>(m.ptr) + r0 * m.ld * 2, m.rows - r0, m.cols, m.ld};
 }
 
+// One main-GEMM launch: 512-wide tiles for rows [0, rows_big) and 256-wide ones below
+// (wide_split), or plain 256-wide tiles.
+runlora_status_t gemm_wide_or_narrow(Ctx& c, const GemmReq& q, cudaStream_t st) {
+  const WideSplit w = wide_split(c, q);
+  static const bool dbg = getenv("RUNLORA_DEBUG_WIDE") != nullptr;
+  if (dbg)
+    fprintf(stderr, "[runlora] main GEMM %dx%dx%d: 512-wide rows %d, est. %.2f vs %.2f (256-wide only)\n", q.M, q.N,
+            q.K1 + q.K2, w.rows_big, w.cost, w.cost_small_only);
+  if (w.rows_big == 0) return gemm(c, q, st);
+  GemmReq r[2] = {q, q};
+  const int rb = std::min(w.rows_big, q.M);
+  r[0].BN = 512;
+  r[0].M = rb;
+  r[0].a.rows = rb;
+  if (r[0].K2 > 0) r[0].a2.rows = rb;
+  r[0].tma_store = true;  // the exposed epilogue: full-line bulk stores
+  int nreq = 1;
+  if (rb < q.M) {
+    r[1].M = q.M - rb;
+    r[1].a = rows_from(q.a, rb);
+    if (q.K2 > 0) r[1].a2 = rows_from(q.a2, rb);
+    r[1].D = static_cast<char*>(q.D) + (int64_t)rb * q.ldd * 2;
+    r[1].tma_store = true;
+    nreq = 2;
+  }
+  std::string err;
+  cudaError_t e = launch_tc_gemm(c, r, nreq, st, &err);
+  if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
+  return RUNLORA_OK;
+}
+
 // Runs a main GEMM (bf16 D = q.D, ld q.ldd), split over K into fp32 slabs in the P region
 // and reduced when main_split says so, or as 512-/256-wide tiles when wide_split says so.
 runlora_status_t main_gemm(Ctx& c, GemmReq q, Bufs& b, cudaStream_t st) {
   const MainSplit ms = main_split(q.M, q.N, q.K1);
   if (ms.splits <= 1) {
-    const WideSplit w = wide_split(c, q);
-    static const bool dbg = getenv("RUNLORA_DEBUG_WIDE") != nullptr;
-    if (dbg)
-      fprintf(stderr, "[runlora] main GEMM %dx%dx%d: 512-wide rows %d, est. %.2f vs %.2f (256-wide only)\n", q.M, q.N,
-              q.K1 + q.K2, w.rows_big, w.cost, w.cost_small_only);
-    if (w.rows_big == 0) return gemm(c, q, st);
-    GemmReq r[2] = {q, q};
-    const int rb = std::min(w.rows_big, q.M);
-    r[0].BN = 512;
-    r[0].M = rb;
-    r[0].a.rows = rb;
-    if (r[0].K2 > 0) r[0].a2.rows = rb;
-    r[0].tma_store = true;  // the exposed epilogue: full-line bulk stores
-    int nreq = 1;
-    if (rb < q.M) {
-      r[1].M = q.M - rb;
-      r[1].a = rows_from(q.a, rb);
-      if (q.K2 > 0) r[1].a2 = rows_from(q.a2, rb);
-      r[1].D = static_cast<char*>(q.D) + (int64_t)rb * q.ldd * 2;
-      r[1].tma_store = true;
-      nreq = 2;
-    }
-    std::string err;
-    cudaError_t e = launch_tc_gemm(c, r, nreq, st, &err);
-    if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
-    return RUNLORA_OK;
+    return gemm_wide_or_narrow(c, q, st);
   }
   void* out = q.D;
   const int64_t ldo = q.ldd;
@@ -1402,6 +1408,14 @@ extern "C" runlora_status_t runlora_debug_gemm(runlora_handle_t h, int M, int N,
   // env RUNLORA_DEBUG_TMA_STORE=1: the TMA-store epilogue (plain bf16 output, 256/512-wide tiles)
   q.tma_store = getenv("RUNLORA_DEBUG_TMA_STORE") && out_mode == OUT_BF16 && q.splits <= 1 && BN >= 256;
   DeviceGuard dg(h->ctx->device());
+  if (BN == 0) {  // the main GEMMs' launch: 512/256-wide split by the planner
+    q.BN = 256;
+    q.cg = 2;
+    q.kid = KID_GEMM_MAIN;
+    if (out_mode != OUT_BF16 || q.splits > 1) return fail(RUNLORA_ERR_INVALID_ARG, "debug_gemm: BN = 0 needs a bf16 output");
+    RL_TRY(gemm_wide_or_narrow(*h->ctx, q, static_cast<cudaStream_t>(stream)));
+    return post_launch();
+  }
   RL_TRY(gemm(*h->ctx, q, static_cast<cudaStream_t>(stream)));
   return post_launch();
 }
