@@ -77,3 +77,44 @@ def test_wide_all_variants_match_oracle(rl, c):
         errs[f"B{b}"] = max(O.rel_fro(_np(dA), wA), O.rel_fro(_np(dB), wB), O.rel_fro(_np(dX), wX))
     assert all(e <= 2e-2 for e in errs.values()), errs
     assert max(errs.values()) < 5e-3, errs
+
+
+_CHILD = r"""
+import sys, torch
+sys.path.insert(0, {root!r})
+import synth
+from paper_2312_03415_b200 import runlora as rl
+c = synth.case("wide_w1", 0, 40, 3000, 2048, 3304, 16, "bf16")
+d = {{k: v.cuda() for k, v in synth.operands(c).items()}}
+h = rl.handle(0)
+shape = rl.make_shape(c.n, c.k, c.m, c.r, rl.BF16)
+Y = torch.empty(c.n, c.m, dtype=torch.bfloat16, device="cuda")
+dX = torch.empty(c.n, c.k, dtype=torch.bfloat16, device="cuda")
+dA = torch.empty(c.k, c.r, device="cuda"); dB = torch.empty(c.r, c.m, device="cuda")
+h.forward(2, shape, d["X"], d["W"], d["A"], d["B"], Y)
+h.backward(1, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], dX, dA, dB)
+torch.save({{"Y": Y.cpu(), "dX": dX.cpu(), "dA": dA.cpu(), "dB": dB.cpu()}}, sys.argv[1])
+"""
+
+
+def test_wide_reduced_stages_bit_exact(tmp_path):
+    """RUNLORA_MAIN_STAGES < 7 (set by bench.py under data parallelism) runs the 512-wide
+    kernel on 3 of its 4 ring stages: same arithmetic, so bit-identical outputs."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "child.py"
+    script.write_text(_CHILD.format(root=root))
+    outs = []
+    for st in ("", "6"):
+        env = dict(os.environ)
+        env.pop("RUNLORA_MAIN_STAGES", None)
+        if st:
+            env["RUNLORA_MAIN_STAGES"] = st
+        f = tmp_path / f"out{st or 'default'}.pt"
+        p = subprocess.run([sys.executable, str(script), str(f)], env=env, capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs.append(torch.load(f))
+    for k in ("Y", "dX", "dA", "dB"):
+        assert torch.equal(outs[0][k], outs[1][k]), k
