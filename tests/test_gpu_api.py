@@ -1,7 +1,6 @@
 """GPU tests of the rest of the public surface: the time/hybrid selector, the autograd
 op, the host-buffer end-to-end step, and the tracing hooks — all through the C ABI and
 checked against the CPU fp64 oracle where they produce numbers."""
-import math
 
 import numpy as np
 import pytest

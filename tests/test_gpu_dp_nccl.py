@@ -5,7 +5,6 @@ overlapped with the dX GEMM (dp.overlapped_backward), and the stack's bucketed s
 its collectives issued from the backward.  A one-rank SUM is the identity, so the results
 must equal the non-distributed ones bit for bit.
 """
-import os
 import socket
 
 import pytest

@@ -6,7 +6,6 @@ compared with an fp64 product of the same bf16 values.
 """
 import ctypes as C
 
-import numpy as np
 import pytest
 import torch
 

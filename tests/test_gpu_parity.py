@@ -6,7 +6,6 @@ Tolerances (BASELINE.json north star): relative Frobenius error <= 1e-5 for fp32
 BASELINE.json configs at full size are compared on sampled rows of Y and dX
 (rows the oracle computes one by one) and in full for dA, dB.
 """
-import numpy as np
 import pytest
 import torch
 

@@ -6,7 +6,6 @@ linear (paper_2312_03415_b200.stack), against the fp64 oracle composition
 (BASELINE.json bf16 tolerance); activations between linears are rounded to bf16 on the
 GPU, so the healthy range here is a few 1e-3.
 """
-import numpy as np
 import pytest
 import torch
 

@@ -5,7 +5,6 @@ a ragged last column tile of one MMA half (N = 3304: 232 columns) and of two hal
 (relative Frobenius <= 2e-2 per tensor, healthy < 5e-3)."""
 import ctypes as C
 
-import numpy as np
 import pytest
 import torch
 
