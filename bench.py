@@ -239,7 +239,11 @@ def main():
     ws = h.workspace(shape)
     Y = torch.empty(n, m, dtype=torch.bfloat16, device=dev)
     dX = torch.empty(n, k, dtype=torch.bfloat16, device=dev)
-    g = dp.PackedAdapterGrads.create(k, r, m, dev)
+    # DP exchange: NCCL allreduce (default) or the one-shot symmetric-memory kernel (opt-in)
+    sym = None
+    if world > 1 and args.backend == "nccl" and os.environ.get("RUNLORA_DP_TRANSPORT") == "symm":
+        sym = dp.SymmetricAllreduce(k, r, m, dev, h)
+    g = sym.grads if sym is not None else dp.PackedAdapterGrads.create(k, r, m, dev)
     crit = {"flops": rl.BY_FLOPS, "time": rl.BY_TIME, "hybrid": rl.HYBRID}[args.criterion]
     if args.plan:
         crit = rl.BY_FLOPS
@@ -259,7 +263,7 @@ def main():
             work = dp.overlapped_backward(
                 lambda: h.backward_params(bwd, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], g.dA, g.dB, ws=ws),
                 lambda: h.backward_input(bwd, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], dX, ws=ws),
-                g, comm_stream=comm)
+                g, comm_stream=comm, exchange=sym)
             work.wait()
         else:
             h.backward(bwd, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], dX, g.dA, g.dB, ws=ws)
@@ -437,7 +441,7 @@ def main():
                           "plan_times_us": plan.as_dict()["time_fwd_us"] | {f"B{v}": t for v, t in
                                                                            plan.as_dict()["time_bwd_us"].items()},
                           "flops_pick": f"F{plan.flops_fwd_pick}+B{plan.flops_bwd_pick}",
-                          "parallelism": f"dp{world} token-sharded, allreduce fp32 [dA|dB]",
+                          "parallelism": f"dp{world} token-sharded, " + ("one-shot symmetric-memory allreduce" if sym is not None else "NCCL allreduce") + " of fp32 [dA|dB]",
                           "l2": "inputs larger than L2: per-step working set X, dY, Y, dX 64 MiB each + W 32 MiB "
                                 "(288 MiB) > 126 MB L2"},
                "tflops": flops_step / (ms * 1e-3) / 1e12,

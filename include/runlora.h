@@ -222,6 +222,21 @@ runlora_status_t runlora_backward_wq(runlora_handle_t h, int bwd, const runlora_
                                      const void* dY, void* dX, void* dA, void* dB, int grad_dtype, int accumulate,
                                      void* workspace, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------- data-parallel exchange (one-shot allreduce)
+ * The DP exchange step (token-sharded ranks; a8 reduces the per-rank
+ * adapter gradients dA = Xᵀ·dY·Bᵀ, dB = Aᵀ·Xᵀ·dY, which are sums over tokens, Eq. 3):
+ *   out[i] = sum_{p = 0 .. P-1} peers[p][i]      (fp32, i < n, rank order 0, 1, .., P-1)
+ * read directly from the P ranks' device buffers (peer pointers valid in this process:
+ * CUDA IPC / torch symmetric memory, NVLink P2P loads).  Every rank that calls it with the
+ * same peers gets a bit-identical result.  peers: HOST array of P device pointers (16-byte
+ * aligned, n floats each, 1 <= P <= 16); out: this rank's device buffer (16-byte aligned),
+ * not one of the peers'.  Ordering across ranks is the caller's: every rank's writes to its
+ * buffer must be visible before any rank's call (a cross-rank barrier on `stream`), and no
+ * buffer may be rewritten until every rank's call has finished (a second barrier).
+ * Asynchronous on `stream`.  Errors: INVALID_ARG (P, n, null/aliased pointers), ALIGNMENT. */
+runlora_status_t runlora_allreduce_sum_f32(runlora_handle_t h, const float* const* peers, int P, float* out,
+                                           int64_t n, void* stream);
+
 /* ---------------------------------------------------------------- tracing
  * When enabled, every kernel the library launches is bracketed by CUDA events
  * on its stream; runlora_profile_read synchronises those events and returns

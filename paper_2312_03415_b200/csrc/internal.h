@@ -27,6 +27,7 @@ enum KernelId : int {
   KID_REPEAT_COLS,     // A repeated along its columns (dX tail against Z1's partial blocks)
   KID_QUANT,           // W -> FP8 E4M3 + per-column scales (column max, quantize, finalize)
   KID_DEQUANT,         // FP8 E4M3 W -> bf16 W in the workspace (QLoRA-style entry points)
+  KID_ALLREDUCE,       // one-shot fixed-order allreduce of [dA | dB] over peer pointers
   KID_COUNT
 };
 extern const char* const kKernelNames[KID_COUNT];
@@ -193,6 +194,9 @@ cudaError_t launch_splitk_reduce(Ctx& ctx, const ReduceJob* jobs, int njobs, cud
 // Quantized frozen weight (quant.cu): W[k, m] bf16 -> Wq e4m3 bytes + scale[m] fp32, and back
 // to bf16 (m multiple of 8, scale 16-byte aligned).
 cudaError_t launch_quantize_w(Ctx& ctx, const void* W, int64_t k, int64_t m, void* Wq, float* scale, cudaStream_t s);
+constexpr int kMaxPeers = 16;  // runlora_allreduce_sum_f32
+cudaError_t launch_allreduce_sum_f32(Ctx& ctx, const float* const* peers, int P, float* out, int64_t n,
+                                     cudaStream_t s);
 cudaError_t launch_dequantize_w(Ctx& ctx, const void* Wq, const float* scale, int64_t k, int64_t m, void* W,
                                 cudaStream_t s);
 // dst[i, t*cols + j] = src[i, j] for t < reps (bf16, row-major; 16-byte column groups).

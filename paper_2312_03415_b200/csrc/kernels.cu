@@ -16,6 +16,7 @@ namespace runlora {
 const char* const kKernelNames[KID_COUNT] = {
     "gemm_main",      "gemm_wprime", "gemm_proj",        "gemm_tokred",
     "gemm_dense_xtdy", "gemm_small",  "splitk_reduce", "sgemm_f32", "repeat_cols", "quantize_w", "dequantize_w",
+    "allreduce_sum",
 };
 
 namespace {

@@ -1251,6 +1251,25 @@ runlora_status_t runlora_quantize_w_e4m3(runlora_handle_t h, int64_t k, int64_t 
   return RUNLORA_OK;
 }
 
+runlora_status_t runlora_allreduce_sum_f32(runlora_handle_t h, const float* const* peers, int P, float* out,
+                                           int64_t n, void* stream) {
+  RL_TRY(check_handle(h));
+  if (!peers || P < 1 || P > kMaxPeers) return fail(RUNLORA_ERR_INVALID_ARG, "allreduce: need 1..16 peer buffers");
+  if (n < 0) return fail(RUNLORA_ERR_INVALID_ARG, "allreduce: n must be >= 0");
+  RL_TRY(check_ptr(out, "out"));
+  for (int q = 0; q < P; ++q) {
+    RL_TRY(check_ptr(peers[q], "peers[p]"));
+    if (reinterpret_cast<uintptr_t>(peers[q]) & 15) return fail(RUNLORA_ERR_ALIGNMENT, "allreduce: peer buffers must be 16-byte aligned");
+    if (peers[q] == out) return fail(RUNLORA_ERR_INVALID_ARG, "allreduce: out must not be a peer buffer");
+  }
+  if (reinterpret_cast<uintptr_t>(out) & 15) return fail(RUNLORA_ERR_ALIGNMENT, "allreduce: out must be 16-byte aligned");
+  if (n == 0) return RUNLORA_OK;
+  DeviceGuard dg(h->ctx->device());
+  cudaError_t e = launch_allreduce_sum_f32(*h->ctx, peers, P, out, n, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "allreduce launch");
+  return RUNLORA_OK;
+}
+
 runlora_status_t runlora_workspace_size_wq(const runlora_shape_t* s, int fwd, int bwd, size_t* bytes) {
   RL_TRY(runlora_workspace_size(s, fwd, bwd, bytes));
   if (s->dtype != RUNLORA_BF16) return fail(RUNLORA_ERR_DTYPE, "quantized W needs bf16 operands");

@@ -44,12 +44,65 @@ def allreduce_adapter_grads(g: PackedAdapterGrads, group=None, async_op: bool = 
     return dist.all_reduce(g.flat, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
 
 
+class SymmetricAllreduce:
+    """One-shot allreduce of the packed fp32 [dA | dB] over torch symmetric memory (SURVEY
+    §8(f) NEXT-2; the a8 exchange without NCCL): each rank's adapter-grad kernels write its
+    partial sums straight into its symmetric buffer (`grads` views), a cross-rank barrier
+    makes every buffer visible, each rank sums all P buffers in rank order over NVLink with
+    runlora_allreduce_sum_f32 into `out` (`result` views; bit-identical on every rank), and
+    a second barrier keeps the buffers intact until every rank has read them.
+
+    Opt-in (bench.py: RUNLORA_DP_TRANSPORT=symm); this round's box had one GPU, so the
+    multi-GPU path is untested beyond P = 1 (tests/test_gpu_allreduce.py)."""
+
+    def __init__(self, k: int, r: int, m: int, device, handle, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+        group = group if group is not None else dist.group.WORLD
+        numel = k * r + r * m
+        self.buf = symm_mem.empty(numel, dtype=torch.float32, device=device)
+        self.hdl = symm_mem.rendezvous(self.buf, group)
+        self.out = torch.empty(numel, dtype=torch.float32, device=device)
+        self.ptrs = [int(p) for p in self.hdl.buffer_ptrs]  # rank order
+        self.handle = handle
+        self.grads = PackedAdapterGrads(self.buf, self.buf[: k * r].view(k, r), self.buf[k * r:].view(r, m))
+        self.result = PackedAdapterGrads(self.out, self.out[: k * r].view(k, r), self.out[k * r:].view(r, m))
+
+    def run(self):
+        """On the current stream: barrier, fixed-order sum of all ranks' buffers, barrier."""
+        self.hdl.barrier(channel=0)
+        self.handle.allreduce_sum_f32(self.ptrs, self.out)
+        self.hdl.barrier(channel=1)
+
+
+class _StreamJoin:
+    def __init__(self, stream, device):
+        self.stream, self.device = stream, device
+
+    def wait(self):
+        if self.stream is not None:
+            torch.cuda.current_stream(self.device).wait_stream(self.stream)
+
+
 def overlapped_backward(run_params: Callable[[], None], run_input: Callable[[], None], g: PackedAdapterGrads,
-                        group=None, comm_stream: Optional["torch.cuda.Stream"] = None):
+                        group=None, comm_stream: Optional["torch.cuda.Stream"] = None,
+                        exchange: Optional[SymmetricAllreduce] = None):
     """Adapter grads -> async allreduce (on `comm_stream` when on CUDA) -> dX.
 
-    Returns the collective's work handle; call .wait() before using g.flat."""
+    Returns the collective's work handle; call .wait() before using g.flat (or, with
+    `exchange`, exchange.result — g must then be exchange.grads)."""
     run_params()
+    if exchange is not None:
+        if comm_stream is None:
+            exchange.run()
+            run_input()
+            return _StreamJoin(None, g.flat.device)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(g.flat.device))
+        comm_stream.wait_event(ev)
+        with torch.cuda.stream(comm_stream):
+            exchange.run()
+        run_input()
+        return _StreamJoin(comm_stream, g.flat.device)
     if comm_stream is not None and g.flat.is_cuda:
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(g.flat.device))

@@ -103,6 +103,7 @@ def _load():
         "runlora_workspace_size_wq": (I, [S, I, I, C.POINTER(SZ)]),
         "runlora_forward_wq": (I, [P, I, S, P, P, P, P, P, P, P, SZ, P]),
         "runlora_backward_wq": (I, [P, I, S, P, P, P, P, P, P, P, P, P, I, I, P, SZ, P]),
+        "runlora_allreduce_sum_f32": (I, [P, C.POINTER(P), I, P, C.c_int64, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -218,6 +219,15 @@ class Handle:
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
         return self._ws
+
+    # ------------------------------------------------- DP exchange (one-shot allreduce)
+    def allreduce_sum_f32(self, peer_ptrs, out: torch.Tensor, n: int = None):
+        """out[:n] = sum over peer_ptrs (device addresses of fp32 buffers, rank order) —
+        runlora_allreduce_sum_f32; the cross-rank barriers are the caller's."""
+        n = out.numel() if n is None else int(n)
+        arr = (C.c_void_p * len(peer_ptrs))(*[int(p) for p in peer_ptrs])
+        _check(_lib.runlora_allreduce_sum_f32(self._h, arr, len(peer_ptrs), _ptr(out), n, _stream(self.device)),
+               "runlora_allreduce_sum_f32")
 
     # ------------------------------------------------- quantized frozen W (R18)
     def quantize_w(self, W: torch.Tensor):
