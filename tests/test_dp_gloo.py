@@ -100,3 +100,20 @@ def test_packed_grads_are_views():
     g.dA.fill_(1.0)
     g.dB.fill_(2.0)
     assert g.flat[:6].eq(1).all() and g.flat[6:].eq(2).all() and g.flat.numel() == 16
+
+
+def test_overlapped_backward_exchange_order():
+    """With a peer-memory exchange (dp.SymmetricAllreduce, duck-typed here: it needs CUDA),
+    overlapped_backward runs adapter grads, then the exchange, then dX, and returns a
+    waitable handle (host logic only; the kernel is tests/test_gpu_allreduce.py)."""
+    calls = []
+
+    class FakeExchange:
+        def run(self):
+            calls.append("exchange")
+
+    g = dp.PackedAdapterGrads.create(4, 2, 3, "cpu")
+    work = dp.overlapped_backward(lambda: calls.append("params"), lambda: calls.append("input"), g,
+                                  exchange=FakeExchange())
+    work.wait()
+    assert calls == ["params", "exchange", "input"]
