@@ -141,7 +141,7 @@ class Ctx {
   void* identity_ = nullptr;
   bool tma_store_main_ = false;   // env RUNLORA_TMA_STORE_MAIN=1
   bool main_wide_ = true;
-  double wide_cost_a_ = 1.69, wide_cost_e_ = 579.0;
+  double wide_cost_a_ = 1.66, wide_cost_e_ = 443.0;
   std::map<std::tuple<int, int, int, int>, int> wide_cache_;  // (M, N, K, raster) -> rows_big
   int main_stages_ = 0;
   bool tma_store_wprime_ = true;  // env RUNLORA_TMA_STORE_WPRIME=0

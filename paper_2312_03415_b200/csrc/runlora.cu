@@ -531,8 +531,8 @@ runlora_status_t wprime_t_bf16(Ctx& c, const runlora_shape_t& s, const void* W, 
 // the rest as 256-wide ones in the same launch (two problems).  rows_big minimises the
 // busiest pair's summed unit cost under the kernel's static round-robin assignment (unit u
 // -> pair u mod 74).  Cost of a 512-wide tile in 256-wide tile times: a + e / K, fitted to
-// gemm_bench runs at K = 2048 / 4096 / 11008 (1.95 / 1.83 / 1.74: a = 1.69, e = 579 — the
-// exposed epilogue, ~3.7 µs, against a 256-wide tile's ~6.3 ns per K).  Cached per shape.
+// gemm_bench runs at K = 2048 / 4096 (1.87 / 1.77: a = 1.66, e = 443 — the exposed epilogue,
+// ~2.8 µs, against a 256-wide tile's ~6.4 ns per K).  Cached per shape.
 struct WideSplit {
   int rows_big;  // multiple of 256; 0 = no 512-wide tiles
   double cost, cost_small_only;

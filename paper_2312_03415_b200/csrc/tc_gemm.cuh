@@ -257,6 +257,29 @@ __device__ __forceinline__ void stage_store_chunk(const uint32_t (&v)[2][32], ui
   ++st_it;
 }
 
+// As stage_store_chunk for a chunk already packed to bf16 pairs (pk[x] = columns 2x, 2x+1).
+template <int NB>
+__device__ __forceinline__ void stage_store_packed(const uint32_t (&pk)[32], uint8_t* stg, int& st_it, int lane,
+                                                   const CUtensorMap* dmap, int col, int row0) {
+  const int buf = st_it % NB;
+  if (st_it >= NB) {
+    if (lane == 0) bulk_wait_read<NB - 1>();
+    __syncwarp();
+  }
+  uint8_t* rowp = stg + buf * 4096 + lane * 128;
+  const uint32_t sw = (uint32_t)lane & 7u;
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+    *reinterpret_cast<uint4*>(rowp + ((e ^ sw) << 4)) = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+  fence_proxy_async_shared();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(dmap, stg + buf * 4096, col, row0);
+    bulk_commit();
+  }
+  ++st_it;
+}
+
 // EPI = 0: epilogue stores from registers; EPI = 3: TMA-store epilogue (plain bf16 outputs).
 // KS: 64-wide K atoms per pipeline stage (TileCfg).
 template <int BN_MAX, int CG, int OCC = 1, int EPI = 0, int KS = 1>
@@ -535,6 +558,61 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       const int n0 = t.n_blk * p.bn;
       const int row = (g.dbg == 3) ? 0x7fffffff : m0 + q * 32 + lane;
       const int nh = BN_MAX > SLOT_W ? unit_halves(p, t.n_blk, SLOT_W) : 1;
+      if constexpr (BN_MAX > SLOT_W && EPI == 3) {
+        if (nh == 2 && g.dbg != 4) {
+          // 512-wide tile: slot A (tile columns [0, 256)) is read into registers as bf16 and
+          // released at once, so the next tile's MMA 0 starts while slot B (columns
+          // [256, 512)) is staged and stored; slot A's rows are stored last.
+          const int sA = sc & 1, sB = sA ^ 1;
+          uint8_t* stg = smem + STAGES * C::STAGE_BYTES + q * (C::STG_BUFS * 4096);
+          const CUtensorMap* dmap = &tm.m[t.prob][4];
+          const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+          uint32_t held[4][32];  // 4 chunks x 64 columns, bf16 pairs
+          mbar_wait(&tfull[sA], (sA ? use1 : use0) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t v[2][32];
+            tmem_ld_32x32b_x32(t_lane + (uint32_t)(sA * SLOT_W + 64 * c), v[0]);
+            tmem_ld_32x32b_x32(t_lane + (uint32_t)(sA * SLOT_W + 64 * c + 32), v[1]);
+            tmem_ld_wait();
+            reg_fence32(v[0]);
+            reg_fence32(v[1]);
+#pragma unroll
+            for (int x = 0; x < 32; ++x)
+              held[c][x] = pack_bf16x2(__uint_as_float(v[x >> 4][2 * (x & 15)]), __uint_as_float(v[x >> 4][2 * (x & 15) + 1]));
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote<CG>(&tempty[sA], 0);
+          if (sA) ++use1;
+          else ++use0;
+          mbar_wait(&tfull[sB], (sB ? use1 : use0) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            if (n0 + SLOT_W + 64 * c >= p.N) break;  // warp-uniform
+            uint32_t v[2][32];
+            tmem_ld_32x32b_x32(t_lane + (uint32_t)(sB * SLOT_W + 64 * c), v[0]);
+            tmem_ld_32x32b_x32(t_lane + (uint32_t)(sB * SLOT_W + 64 * c + 32), v[1]);
+            tmem_ld_wait();
+            reg_fence32(v[0]);
+            reg_fence32(v[1]);
+            stage_store_chunk<C::STG_BUFS>(v, stg, st_it, lane, dmap, n0 + SLOT_W + 64 * c, m0 + q * 32);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote<CG>(&tempty[sB], 0);
+          if (sB) ++use1;
+          else ++use0;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (n0 + 64 * c < p.N) stage_store_packed<C::STG_BUFS>(held[c], stg, st_it, lane, dmap, n0 + 64 * c, m0 + q * 32);
+          sc += 2;
+          if (g.trace && threadIdx.x == 4 * 32) g.trace[8 * u + 3] = globaltimer();
+          continue;
+        }
+      }
       for (int h = 0; h < nh; ++h) {  // slot by slot: the first is released while the second drains
         const int sl = (sc & 1) ^ h;
         mbar_wait(&tfull[sl], (sl ? use1 : use0) & 1);
@@ -549,40 +627,17 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
           // chunks, STG_BUFS staging tiles per warp: a buffer is reused only after the store
           // issued STG_BUFS chunks earlier has finished reading it.
           uint8_t* stg = smem + STAGES * C::STAGE_BYTES + q * (C::STG_BUFS * 4096);
-          // software pipelined: the TMEM loads of chunk i+1 are in flight while chunk i is
-          // packed, staged and stored
           const int nch = min(bw, p.N - nc + 63) / 64;  // 64-column chunks inside N
           const CUtensorMap* dmap = &tm.m[t.prob][4];
-          uint32_t va[2][32], vb[2][32];
-          if (nch > 0) {
-            tmem_ld_32x32b_x32(t_row, va[0]);
-            tmem_ld_32x32b_x32(t_row + 32, va[1]);
-            tmem_ld_wait();
-            reg_fence32(va[0]);
-            reg_fence32(va[1]);
-          }
 #pragma unroll 1
-          for (int i = 0; i < nch; i += 2) {
-            if (i + 1 < nch) {
-              tmem_ld_32x32b_x32(t_row + 64 * (i + 1), vb[0]);
-              tmem_ld_32x32b_x32(t_row + 64 * (i + 1) + 32, vb[1]);
-            }
-            stage_store_chunk<C::STG_BUFS>(va, stg, st_it, lane, dmap, nc + 64 * i, m0 + q * 32);
-            if (i + 1 < nch) {
-              tmem_ld_wait();
-              reg_fence32(vb[0]);
-              reg_fence32(vb[1]);
-              if (i + 2 < nch) {
-                tmem_ld_32x32b_x32(t_row + 64 * (i + 2), va[0]);
-                tmem_ld_32x32b_x32(t_row + 64 * (i + 2) + 32, va[1]);
-              }
-              stage_store_chunk<C::STG_BUFS>(vb, stg, st_it, lane, dmap, nc + 64 * (i + 1), m0 + q * 32);
-              if (i + 2 < nch) {
-                tmem_ld_wait();
-                reg_fence32(va[0]);
-                reg_fence32(va[1]);
-              }
-            }
+          for (int i = 0; i < nch; ++i) {
+            uint32_t v[2][32];
+            tmem_ld_32x32b_x32(t_row + 64 * i, v[0]);
+            tmem_ld_32x32b_x32(t_row + 64 * i + 32, v[1]);
+            tmem_ld_wait();
+            reg_fence32(v[0]);
+            reg_fence32(v[1]);
+            stage_store_chunk<C::STG_BUFS>(v, stg, st_it, lane, dmap, nc + 64 * i, m0 + q * 32);
           }
         } else if (p.out_mode == OUT_F32_FOLD) {
           // sum of the fold column blocks (w = fold_w in {8, 16, 32}), in block order
