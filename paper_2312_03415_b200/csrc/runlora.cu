@@ -580,9 +580,12 @@ WideSplit wide_split(Ctx& c, const GemmReq& q) {
   w.cost = w.cost_small_only;
   // the 256-wide remainder only ever needs to fill the last round or two
   const int lo = std::max(1, mt - (3 * pairs + nts - 1) / nts);
+  // from all-wide down; a narrower split must win clearly (4 %): in a mixed launch the
+  // 256-wide tiles cost more than the model's 1.0 (C3 8192x11008x4096: model 17.15 vs 17.68
+  // rounds for 27 wide row tiles vs all 32, measured 480.3 vs 472.1 µs)
   for (int rb = mt; rb >= lo; --rb) {
     const double t = simulate(rb);
-    if (t < w.cost * 0.995) w.cost = t, w.rows_big = rb * 256;
+    if (t < w.cost * (w.rows_big ? 0.96 : 0.995)) w.cost = t, w.rows_big = rb * 256;
   }
   cache[key] = w.rows_big;
   return w;
