@@ -330,7 +330,7 @@ def main():
     p_sus = peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"]
     roof = {"bound": "tensor", "achieved": achieved, "peak": p_sus, "unit": "TFLOP/s",
             "frac": achieved / p_sus if achieved else None, "traffic": traffic,
-            "kernel": "gemm_main (tcgen05 Y / dX GEMM)",
+            "kernel": "gemm_main (tcgen05 Y / dX GEMM, 256x512 + 256x256 pair tiles)",
             "peak_source": f"of {peak_src}: bf16 sustained (cuBLAS, seconds-long loop under the power cap)",
             "peak_burst": peaks["bf16_tflops"], "frac_of_burst": achieved / peaks["bf16_tflops"] if achieved else None,
             "flops_per_launch": flops_per_launch}
