@@ -117,3 +117,27 @@ def test_wide_reduced_stages_bit_exact(tmp_path):
         outs.append(torch.load(f))
     for k in ("Y", "dX", "dA", "dB"):
         assert torch.equal(outs[0][k], outs[1][k]), k
+
+
+def test_wide_outputs_stay_in_bounds(rl):
+    """Y and dX live inside larger buffers filled with a sentinel: the wide/narrow launches
+    (ragged rows and a ragged last column tile) must not write outside [0, n·m)."""
+    c = CASES[0]
+    ops = synth.operands(c)
+    d = {k: v.cuda() for k, v in ops.items()}
+    h = rl.handle(0)
+    shape = rl.make_shape(c.n, c.k, c.m, c.r, rl.BF16)
+    pad = 4096
+    sentinel = torch.tensor(-12345.0, dtype=torch.bfloat16)
+    ybuf = torch.full((c.n * c.m + 2 * pad,), sentinel.item(), dtype=torch.bfloat16, device="cuda")
+    xbuf = torch.full((c.n * c.k + 2 * pad,), sentinel.item(), dtype=torch.bfloat16, device="cuda")
+    Y = ybuf[pad:pad + c.n * c.m].view(c.n, c.m)
+    dX = xbuf[pad:pad + c.n * c.k].view(c.n, c.k)
+    dA = torch.empty(c.k, c.r, device="cuda")
+    dB = torch.empty(c.r, c.m, device="cuda")
+    h.forward(2, shape, d["X"], d["W"], d["A"], d["B"], Y)
+    h.backward(1, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], dX, dA, dB)
+    torch.cuda.synchronize()
+    for buf, n_in in ((ybuf, c.n * c.m), (xbuf, c.n * c.k)):
+        assert bool((buf[:pad] == sentinel.item()).all()) and bool((buf[pad + n_in:] == sentinel.item()).all())
+        assert not bool((buf[pad:pad + n_in] == sentinel.item()).any())  # every element written
