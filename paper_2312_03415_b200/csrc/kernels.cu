@@ -116,6 +116,7 @@ cudaError_t dispatch_tc(Ctx& ctx, int bn_max, int cg, bool occ2, bool tma_store,
       case 32: return run_tc<32, 1, 2>(ctx, tm, g, s);
       case 48: return run_tc<48, 1, 2>(ctx, tm, g, s);
       case 64: return run_tc<64, 1, 2>(ctx, tm, g, s);
+      case 128: return run_tc<128, 1, 2>(ctx, tm, g, s);
       default: break;
     }
   }
@@ -379,7 +380,10 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
   for (int q = nreq; q < kMaxProb; ++q) g.p[q] = g.p[0], g.p[q].units = 0;
   if (g.total_units <= 0) return cudaSuccess;
   ctx.launch_begin(s, reqs[0].kid);
-  cudaError_t e = dispatch_tc(ctx, bn_max, cg, ctx.occ2() && reqs[0].a_stream_once, tma_store, tm, g, s);
+  // 2 CTAs per SM for the HBM-bound rank-r kernels; at 128 columns only for the token
+  // reductions (r = 128: 42.6 -> 31.0 µs; the projections lost 38 -> 45 µs to the shallower ring)
+  const bool occ2 = ctx.occ2() && reqs[0].a_stream_once && (bn_max <= 64 || reqs[0].kid == KID_GEMM_TOKRED);
+  cudaError_t e = dispatch_tc(ctx, bn_max, cg, occ2, tma_store, tm, g, s);
   ctx.launch_end(s);
   if (e != cudaSuccess && err) *err = std::string("tc_gemm launch: ") + cudaGetErrorString(e);
   return e;
