@@ -62,6 +62,8 @@ struct GemmReq {
   bool tail_diag;  // a2 = 128x128 identity, b2 read at the tile's own rows (see Prob)
   int a_policy;      // L2 policy of the A operand: 0 from a_stream_once, 1 normal, 2 evict-first
   bool tma_store;  // OUT_BF16 through the TMA-store epilogue (all problems of a launch alike)
+  bool overlaps_comm;  // the dX GEMM, which a data-parallel allreduce overlaps: runs on
+                       // RUNLORA_MAIN_STAGES (fewer ring stages leave shared memory for NCCL)
 };
 
 struct ReduceJob {

@@ -371,7 +371,7 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
   g.nprob = nreq;
   g.trace = (ctx.trace && ctx.trace_kid == reqs[0].kid && g.total_units <= Ctx::kTraceUnits) ? ctx.trace : nullptr;
   g.ltrace = ctx.ltrace_slot(reqs[0].kid);
-  g.stages = reqs[0].kid == KID_GEMM_MAIN ? ctx.main_stages() : 0;
+  g.stages = (reqs[0].kid == KID_GEMM_MAIN && reqs[0].overlaps_comm) ? ctx.main_stages() : 0;
   // RUNLORA_MAIN_STAGES < 7 asks the main GEMMs to leave shared memory for co-resident
   // kernels (NCCL's during an overlapped allreduce): the 512-wide kernel's 48 KB stages then
   // drop from 4 to 3 (frees 48 KB) instead of being clamped to the full ring

@@ -833,6 +833,7 @@ runlora_status_t input_bf16(Ctx& c, int v, const runlora_shape_t& s, const void*
                             const void* dY, void* dX, Bufs& b, cudaStream_t st) {
   const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
   GemmReq q = main_req(c, (int)n, (int)k);
+  q.overlaps_comm = true;  // backward_input runs while backward_params' allreduce is in flight
   q.a = mat(dY, n, m);
   q.a_mn = false;
   q.b_mn = false;
