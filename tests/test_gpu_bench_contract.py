@@ -42,3 +42,20 @@ def test_reference_arm_contract():
     assert d["impl"] == "reference" and d["value"] > 0 and d["dtype"] == "f64"
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_bench_two_ranks_gloo_code_path():
+    """bench.py's data-parallel path (token shards, plan broadcast, overlapped exchange, the
+    dX GEMM on the reduced ring) under torchrun with 2 ranks on this box's one GPU; the
+    exchange uses gloo (CPU), so no rank's GPU kernel waits on another's.  Checks the JSON
+    line, not the numbers (two ranks share one GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29573", os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--backend", "gloo", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+    assert d["config"]["parallelism"].startswith("dp2")
