@@ -39,11 +39,12 @@
  * bf16, k, m and r must be multiples of 8 (TMA needs 16-byte row strides) —
  * otherwise RUNLORA_ERR_ALIGNMENT.
  *
- * Concurrency: a handle may be driven from ONE host thread at a time.  Calls for
- * different streams may be interleaved from that thread if every stream uses its
- * own workspace.  Every launch of a call goes to the caller's stream (one
- * programmatic-dependent-launch chain, no internal streams or events).  Use one
- * handle per host thread otherwise.
+ * Concurrency: any host thread may call into a handle; the calls that enqueue
+ * work or touch the handle's caches are serialised by a per-handle mutex (held
+ * only while the call enqueues; time-mode selection holds it while it measures).
+ * Calls for different streams may run concurrently on the device if every stream
+ * uses its own workspace.  Every launch of a call goes to the caller's stream (one
+ * programmatic-dependent-launch chain, no internal streams or events).
  *
  * Errors: a non-zero runlora_status_t; runlora_last_error() returns a
  * thread-local message naming the offending argument(s).  No C++ exception
@@ -60,7 +61,7 @@
 extern "C" {
 #endif
 
-#define RUNLORA_ABI_VERSION 1
+#define RUNLORA_ABI_VERSION 2
 
 typedef enum {
   RUNLORA_OK = 0,
@@ -184,9 +185,14 @@ runlora_status_t runlora_backward_input(runlora_handle_t h, int bwd, const runlo
 
 /* End-to-end step from HOST buffers: H2D copies of X_host and dY_host into the
  * device staging buffers X, dY; forward(fwd) into Y; backward(bwd) into dX, dA,
- * dB; D2H copies of dA, dB into dA_host, dB_host (and of Y / dX when Y_host /
- * dX_host are non-NULL).  Everything is enqueued on `stream`; the call returns
- * without synchronising.  W, A, B are device pointers (resident parameters). */
+ * dB; then, if `exchange` is non-NULL, exchange(exchange_user, stream) is called on
+ * the calling thread (the data-parallel allreduce of dA, dB is enqueued there, so
+ * the host copies below receive the summed gradients); then D2H copies of dA, dB
+ * into dA_host, dB_host (and of Y / dX when Y_host / dX_host are non-NULL).
+ * Everything is enqueued on `stream`; the call returns without synchronising.
+ * W, A, B are device pointers (resident parameters).  Every argument (variants,
+ * pointers, workspace) is validated before the first copy is enqueued. */
+typedef void (*runlora_exchange_fn)(void* user, void* stream);
 typedef struct {
   int32_t fwd, bwd, grad_dtype, accumulate;
   const void *X_host, *dY_host;          /* host inputs  */
@@ -194,6 +200,8 @@ typedef struct {
   void *dA_host, *dB_host;               /* host outputs */
   const void *W, *A, *B;                 /* device parameters */
   void *X, *dY, *Y, *dX, *dA, *dB;       /* device staging buffers */
+  runlora_exchange_fn exchange;          /* nullable (ABI version 2) */
+  void* exchange_user;
 } runlora_host_step_t;
 runlora_status_t runlora_step_host(runlora_handle_t h, const runlora_shape_t* s, const runlora_host_step_t* st,
                                    void* workspace, size_t ws_bytes, void* stream);

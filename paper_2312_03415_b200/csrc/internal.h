@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <map>
 #include <mutex>
@@ -131,10 +132,15 @@ class Ctx {
   void launch_end(cudaStream_t s);
   void profile_enable(bool on);
   bool profile_read(runlora_kernel_stat_t* stats, int max_stats, int* count, bool reset, std::string* err);
-  uint64_t launches() const { return launches_; }
+  uint64_t launches() const { return launches_.load(); }
 
   std::mutex plan_mu;
   std::map<std::vector<int64_t>, runlora_plan_t> plans;
+  // Serialises every ABI call that enqueues work or touches the caches below (deferred
+  // reducer jobs, wide-tile plans, launch-trace slots, profiling events): any host thread
+  // may call into a handle (e.g. autograd runs the backward on its own thread).  Recursive:
+  // time-mode selection and runlora_step_host call the forward/backward entry points.
+  std::recursive_mutex call_mu;
 
  private:
   int device_;
@@ -171,7 +177,7 @@ class Ctx {
   std::mutex tmap_mu_;
   std::unordered_map<TmapKey, CUtensorMap, TmapKeyHash> tmaps_;
   bool profiling_ = false;
-  uint64_t launches_ = 0;
+  std::atomic<uint64_t> launches_{0};
   struct Pending {
     KernelId kid;
     cudaEvent_t a, b;

@@ -924,8 +924,10 @@ runlora_status_t post_launch() {
   return RUNLORA_OK;
 }
 
-runlora_status_t do_forward(runlora_handle_t h, int fwd, const runlora_shape_t* s, const void* X, const void* W,
-                            const void* A, const void* B, void* Y, void* ws, size_t ws_bytes, void* stream) {
+using CallLock = std::lock_guard<std::recursive_mutex>;
+
+runlora_status_t validate_forward(runlora_handle_t h, int fwd, const runlora_shape_t* s, const void* X, const void* W,
+                                  const void* A, const void* B, const void* Y) {
   RL_TRY(check_handle(h));
   RL_TRY(check_shape(s));
   if (fwd != 1 && fwd != 2) return fail(RUNLORA_ERR_INVALID_ARG, "forward variant must be 1 or 2 (P:62-64)");
@@ -934,8 +936,15 @@ runlora_status_t do_forward(runlora_handle_t h, int fwd, const runlora_shape_t* 
   RL_TRY(check_ptr(A, "A"));
   RL_TRY(check_ptr(B, "B"));
   RL_TRY(check_ptr(Y, "Y"));
+  return RUNLORA_OK;
+}
+
+runlora_status_t do_forward(runlora_handle_t h, int fwd, const runlora_shape_t* s, const void* X, const void* W,
+                            const void* A, const void* B, void* Y, void* ws, size_t ws_bytes, void* stream) {
+  RL_TRY(validate_forward(h, fwd, s, X, W, A, B, Y));
   Bufs b;
   RL_TRY(bind_ws(*s, ws, ws_bytes, &b));
+  CallLock lk(h->ctx->call_mu);
   DeviceGuard dg(h->ctx->device());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (s->dtype == RUNLORA_BF16) RL_TRY(forward_bf16(*h->ctx, fwd, *s, X, W, A, B, Y, b, st));
@@ -953,11 +962,10 @@ runlora_status_t check_bwd_common(runlora_handle_t h, int bwd, const runlora_sha
   return RUNLORA_OK;
 }
 
-runlora_status_t do_params(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X, const void* W,
-                           const void* A, const void* B, const void* dY, void* dA, void* dB, int grad_dtype,
-                           int accumulate, void* ws, size_t ws_bytes, void* stream, bool defer = false) {
+runlora_status_t validate_params(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X,
+                                 const void* A, const void* B, const void* dY, const void* dA, const void* dB,
+                                 int grad_dtype) {
   RL_TRY(check_bwd_common(h, bwd, s));
-  (void)W;
   RL_TRY(check_ptr(X, "X"));
   RL_TRY(check_ptr(A, "A"));
   RL_TRY(check_ptr(B, "B"));
@@ -967,8 +975,28 @@ runlora_status_t do_params(runlora_handle_t h, int bwd, const runlora_shape_t* s
   if (grad_dtype != RUNLORA_F32 && grad_dtype != RUNLORA_BF16) return fail(RUNLORA_ERR_DTYPE, "grad_dtype must be F32 or BF16");
   if (s->dtype == RUNLORA_F32 && grad_dtype != RUNLORA_F32)
     return fail(RUNLORA_ERR_DTYPE, "fp32 operands need fp32 adapter gradients");
+  return RUNLORA_OK;
+}
+
+runlora_status_t validate_input(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* W, const void* A,
+                                const void* B, const void* dY, const void* dX) {
+  RL_TRY(check_bwd_common(h, bwd, s));
+  RL_TRY(check_ptr(W, "W"));
+  RL_TRY(check_ptr(A, "A"));
+  RL_TRY(check_ptr(B, "B"));
+  RL_TRY(check_ptr(dY, "dY"));
+  RL_TRY(check_ptr(dX, "dX"));
+  return RUNLORA_OK;
+}
+
+runlora_status_t do_params(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X, const void* W,
+                           const void* A, const void* B, const void* dY, void* dA, void* dB, int grad_dtype,
+                           int accumulate, void* ws, size_t ws_bytes, void* stream, bool defer = false) {
+  (void)W;
+  RL_TRY(validate_params(h, bwd, s, X, A, B, dY, dA, dB, grad_dtype));
   Bufs b;
   RL_TRY(bind_ws(*s, ws, ws_bytes, &b));
+  CallLock lk(h->ctx->call_mu);
   DeviceGuard dg(h->ctx->device());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (s->dtype == RUNLORA_BF16)
@@ -981,14 +1009,10 @@ runlora_status_t do_params(runlora_handle_t h, int bwd, const runlora_shape_t* s
 
 runlora_status_t do_input(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* W, const void* A,
                           const void* B, const void* dY, void* dX, void* ws, size_t ws_bytes, void* stream) {
-  RL_TRY(check_bwd_common(h, bwd, s));
-  RL_TRY(check_ptr(W, "W"));
-  RL_TRY(check_ptr(A, "A"));
-  RL_TRY(check_ptr(B, "B"));
-  RL_TRY(check_ptr(dY, "dY"));
-  RL_TRY(check_ptr(dX, "dX"));
+  RL_TRY(validate_input(h, bwd, s, W, A, B, dY, dX));
   Bufs b;
   RL_TRY(bind_ws(*s, ws, ws_bytes, &b));
+  CallLock lk(h->ctx->call_mu);
   DeviceGuard dg(h->ctx->device());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (s->dtype == RUNLORA_BF16) RL_TRY(input_bf16(*h->ctx, bwd, *s, W, A, B, dY, dX, b, st));
@@ -999,6 +1023,14 @@ runlora_status_t do_input(runlora_handle_t h, int bwd, const runlora_shape_t* s,
 runlora_status_t do_backward(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X, const void* W,
                              const void* A, const void* B, const void* dY, void* dX, void* dA, void* dB,
                              int grad_dtype, int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  // Everything is validated before the first launch (the split calls validate again).
+  RL_TRY(validate_params(h, bwd, s, X, A, B, dY, dA, dB, grad_dtype));
+  if (dX) RL_TRY(validate_input(h, bwd, s, W, A, B, dY, dX));
+  {
+    Bufs b;
+    RL_TRY(bind_ws(*s, ws, ws_bytes, &b));
+  }
+  CallLock lk(h->ctx->call_mu);
   // With dX, the adapter-gradient reducer is launched after the dX GEMM on the same stream:
   // it co-resides with the GEMM's last wave and the whole backward stays one
   // programmatic-dependent-launch chain (no cross-stream events).
@@ -1137,6 +1169,7 @@ runlora_status_t runlora_select(runlora_handle_t h, const runlora_shape_t* s, in
     }
   }
   if (!ops) return fail(RUNLORA_ERR_INVALID_ARG, "time-based selection needs device operands");
+  CallLock lk(h->ctx->call_mu);  // the candidates are measured without interleaved calls
   DeviceGuard dg(h->ctx->device());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaEvent_t e0, e1;
@@ -1249,6 +1282,7 @@ runlora_status_t runlora_quantize_w_e4m3(runlora_handle_t h, int64_t k, int64_t 
   RL_TRY(check_ptr(W, "W"));
   RL_TRY(check_ptr(Wq, "Wq"));
   RL_TRY(check_ptr(scale, "scale"));
+  CallLock lk(h->ctx->call_mu);
   DeviceGuard dg(h->ctx->device());
   cudaError_t e = launch_quantize_w(*h->ctx, W, k, m, Wq, scale, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "quantize launch");
@@ -1268,6 +1302,7 @@ runlora_status_t runlora_allreduce_sum_f32(runlora_handle_t h, const float* cons
   }
   if (reinterpret_cast<uintptr_t>(out) & 15) return fail(RUNLORA_ERR_ALIGNMENT, "allreduce: out must be 16-byte aligned");
   if (n == 0) return RUNLORA_OK;
+  CallLock lk(h->ctx->call_mu);
   DeviceGuard dg(h->ctx->device());
   cudaError_t e = launch_allreduce_sum_f32(*h->ctx, peers, P, out, n, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "allreduce launch");
@@ -1300,6 +1335,7 @@ runlora_status_t dequant_into_ws(runlora_handle_t h, const runlora_shape_t* s, c
     return fail(RUNLORA_ERR_WORKSPACE, b);
   }
   void* wdq = static_cast<char*>(ws) + main;
+  CallLock lk(h->ctx->call_mu);
   DeviceGuard dg(h->ctx->device());
   cudaError_t e = launch_dequantize_w(*h->ctx, Wq, scale, s->k, s->m, wdq, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "dequantize launch");
@@ -1335,6 +1371,16 @@ runlora_status_t runlora_step_host(runlora_handle_t h, const runlora_shape_t* s,
   if (!t) return fail(RUNLORA_ERR_INVALID_ARG, "step is NULL");
   if (!t->X_host || !t->dY_host || !t->dA_host || !t->dB_host)
     return fail(RUNLORA_ERR_INVALID_ARG, "X_host, dY_host, dA_host, dB_host must be non-NULL");
+  // everything the forward and backward will check, before the first copy is enqueued
+  RL_TRY(validate_forward(h, t->fwd, s, t->X, t->W, t->A, t->B, t->Y));
+  RL_TRY(validate_params(h, t->bwd, s, t->X, t->A, t->B, t->dY, t->dA, t->dB, t->grad_dtype));
+  if (t->dX) RL_TRY(validate_input(h, t->bwd, s, t->W, t->A, t->B, t->dY, t->dX));
+  if (t->dX_host && !t->dX) return fail(RUNLORA_ERR_INVALID_ARG, "dX_host needs the device buffer dX");
+  {
+    Bufs b;
+    RL_TRY(bind_ws(*s, ws, ws_bytes, &b));
+  }
+  CallLock lk(h->ctx->call_mu);
   DeviceGuard dg(h->ctx->device());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t es = s->dtype == RUNLORA_BF16 ? 2 : 4;
@@ -1348,19 +1394,21 @@ runlora_status_t runlora_step_host(runlora_handle_t h, const runlora_shape_t* s,
   RL_TRY(do_forward(h, t->fwd, s, t->X, t->W, t->A, t->B, t->Y, ws, ws_bytes, stream));
   RL_TRY(do_backward(h, t->bwd, s, t->X, t->W, t->A, t->B, t->dY, t->dX, t->dA, t->dB, t->grad_dtype, t->accumulate,
                      ws, ws_bytes, stream));
+  if (t->exchange) t->exchange(t->exchange_user, stream);  // e.g. the DP allreduce of dA, dB
   if ((e = cudaMemcpyAsync(t->dA_host, t->dA, (size_t)s->k * s->r * ges, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
     return cuda_fail(e, "D2H dA");
   if ((e = cudaMemcpyAsync(t->dB_host, t->dB, (size_t)s->r * s->m * ges, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
     return cuda_fail(e, "D2H dB");
   if (t->Y_host && (e = cudaMemcpyAsync(t->Y_host, t->Y, yb, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
     return cuda_fail(e, "D2H Y");
-  if (t->dX_host && t->dX && (e = cudaMemcpyAsync(t->dX_host, t->dX, xb, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+  if (t->dX_host && (e = cudaMemcpyAsync(t->dX_host, t->dX, xb, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
     return cuda_fail(e, "D2H dX");
   return RUNLORA_OK;
 }
 
 runlora_status_t runlora_profile_enable(runlora_handle_t h, int enable) {
   RL_TRY(check_handle(h));
+  CallLock lk(h->ctx->call_mu);
   h->ctx->profile_enable(enable != 0);
   return RUNLORA_OK;
 }
@@ -1369,6 +1417,7 @@ runlora_status_t runlora_profile_read(runlora_handle_t h, runlora_kernel_stat_t*
                                       int reset) {
   RL_TRY(check_handle(h));
   std::string err;
+  CallLock lk(h->ctx->call_mu);
   DeviceGuard dg(h->ctx->device());
   if (!h->ctx->profile_read(stats, max_stats, count, reset != 0, &err)) return fail(RUNLORA_ERR_CUDA, err);
   return RUNLORA_OK;
@@ -1430,6 +1479,7 @@ extern "C" runlora_status_t runlora_debug_gemm(runlora_handle_t h, int M, int N,
   q.split_stride = (int64_t)M * N;
   // env RUNLORA_DEBUG_TMA_STORE=1: the TMA-store epilogue (plain bf16 output, 256/512-wide tiles)
   q.tma_store = getenv("RUNLORA_DEBUG_TMA_STORE") && out_mode == OUT_BF16 && q.splits <= 1 && BN >= 256;
+  CallLock lk(h->ctx->call_mu);
   DeviceGuard dg(h->ctx->device());
   if (BN == 0) {  // the main GEMMs' launch: 512/256-wide split by the planner
     q.BN = 256;
@@ -1464,12 +1514,14 @@ extern "C" int runlora_debug_trace(runlora_handle_t h, unsigned long long* host,
 // Synchronises the device.  Returns the number of launches copied.
 extern "C" int runlora_debug_ltrace(runlora_handle_t h, unsigned long long* host, int* kids, int max_launches) {
   if (!h || !h->ctx || !host || !kids) return 0;
+  CallLock lk(h->ctx->call_mu);
   DeviceGuard dg(h->ctx->device());
   return h->ctx->ltrace_read(host, kids, max_launches);
 }
 
 extern "C" int runlora_debug_wide_rows(runlora_handle_t h, int M, int N, int K, int b_mn) {
   if (!h || !h->ctx || M <= 0 || N <= 0 || K <= 0) return -1;
+  CallLock lk(h->ctx->call_mu);
   GemmReq q = main_req(*h->ctx, M, N);
   q.K1 = K;
   q.b_mn = b_mn != 0;

@@ -54,13 +54,16 @@ class Operands(C.Structure):
                 ("grad_dtype", C.c_int32)]
 
 
+EXCHANGE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)  # runlora_exchange_fn(user, stream)
+
+
 class HostStep(C.Structure):
     _fields_ = [("fwd", C.c_int32), ("bwd", C.c_int32), ("grad_dtype", C.c_int32), ("accumulate", C.c_int32),
                 ("X_host", C.c_void_p), ("dY_host", C.c_void_p), ("Y_host", C.c_void_p), ("dX_host", C.c_void_p),
                 ("dA_host", C.c_void_p), ("dB_host", C.c_void_p),
                 ("W", C.c_void_p), ("A", C.c_void_p), ("B", C.c_void_p),
                 ("X", C.c_void_p), ("dY", C.c_void_p), ("Y", C.c_void_p), ("dX", C.c_void_p),
-                ("dA", C.c_void_p), ("dB", C.c_void_p)]
+                ("dA", C.c_void_p), ("dB", C.c_void_p), ("exchange", EXCHANGE_FN), ("exchange_user", C.c_void_p)]
 
 
 class KernelStat(C.Structure):
@@ -288,14 +291,19 @@ class Handle:
                                            _ptr(dY), _ptr(dX), _ptr(ws), ws.numel(), _stream(self.device)),
                "runlora_backward_input")
 
-    def step_host(self, shape, fwd, bwd, host: dict, dev: dict, grad_dtype, accumulate=False, ws=None):
+    def step_host(self, shape, fwd, bwd, host: dict, dev: dict, grad_dtype, accumulate=False, ws=None,
+                  exchange=None):
+        """runlora_step_host.  `exchange`: optional callable run after the backward is enqueued
+        and before the D2H copies (e.g. the data-parallel allreduce of dA, dB on the current
+        stream), so the host buffers receive its result."""
         ws = self.workspace(shape) if ws is None else ws
+        cb = EXCHANGE_FN(lambda user, stream: exchange()) if exchange is not None else EXCHANGE_FN()
         st = HostStep(int(fwd), int(bwd), int(grad_dtype), int(bool(accumulate)),
                       _ptr(host["X"]), _ptr(host["dY"]), _ptr(host.get("Y")), _ptr(host.get("dX")),
                       _ptr(host["dA"]), _ptr(host["dB"]),
                       _ptr(dev["W"]), _ptr(dev["A"]), _ptr(dev["B"]),
                       _ptr(dev["X"]), _ptr(dev["dY"]), _ptr(dev["Y"]), _ptr(dev["dX"]), _ptr(dev["dA"]),
-                      _ptr(dev["dB"]))
+                      _ptr(dev["dB"]), cb, None)
         _check(_lib.runlora_step_host(self._h, C.byref(shape), C.byref(st), _ptr(ws), ws.numel(),
                                       _stream(self.device)), "runlora_step_host")
 

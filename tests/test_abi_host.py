@@ -94,3 +94,29 @@ def test_workspace_size_and_validation(rl):
 def test_status_strings(rl):
     for st in range(11):
         assert rl._lib.runlora_status_string(st)
+
+
+def test_null_handle_is_invalid_arg(rl):
+    """Every entry point that takes a handle returns RUNLORA_ERR_INVALID_ARG for NULL before
+    touching anything (include/runlora.h "Errors"); no launch, no dereference."""
+    lib = rl._lib
+    s = rl.make_shape(256, 256, 256, 8, rl.BF16)
+    p = C.c_void_p(4096)  # never dereferenced: the handle check comes first
+    S = C.byref(s)
+    assert lib.runlora_forward(None, 1, S, p, p, p, p, p, p, 1 << 20, None) == 1
+    assert lib.runlora_backward(None, 1, S, p, p, p, p, p, p, p, p, 0, 0, p, 1 << 20, None) == 1
+    assert lib.runlora_backward_params(None, 1, S, p, p, p, p, p, p, p, 0, 0, p, 1 << 20, None) == 1
+    assert lib.runlora_backward_input(None, 1, S, p, p, p, p, p, p, p, 1 << 20, None) == 1
+    st = rl.HostStep(1, 1, 0, 0, *([4096] * 15))
+    assert lib.runlora_step_host(None, S, C.byref(st), p, 1 << 20, None) == 1
+    assert lib.runlora_select(None, S, rl.BY_TIME, None, p, 1 << 20, None, C.byref(rl.Plan())) == 1
+    assert lib.runlora_profile_enable(None, 1) == 1
+    assert "handle" in lib.runlora_last_error().decode()
+
+
+def test_host_step_struct_matches_header(rl):
+    """ABI version 2: runlora_host_step_t ends with the exchange hook (function pointer + user)."""
+    src = open(os.path.join(ROOT, "include", "runlora.h")).read()
+    assert "#define RUNLORA_ABI_VERSION 2" in src
+    assert [f[0] for f in rl.HostStep._fields_][-2:] == ["exchange", "exchange_user"]
+    assert C.sizeof(rl.HostStep) == 4 * 4 + 15 * 8 + 2 * 8

@@ -211,3 +211,79 @@ def test_lora_linear_time_criterion(rl):
     assert O.rel_fro(_np(Y), O.forward(1, Xn, Wn, An, Bn)) <= TOL
     for g, w in ((A.grad, wA), (B.grad, wB), (X.grad, wX)):
         assert O.rel_fro(_np(g), w) <= TOL
+
+
+def test_one_handle_two_threads_two_streams(rl):
+    """One handle driven from two host threads at once, each with its own stream and
+    workspace (as autograd does: forward on the caller's thread, backward on the engine's):
+    the per-handle call lock serialises the enqueues; both results stay parity-green and
+    equal to a single-threaded run bit for bit."""
+    import threading
+    cs = [synth.case("thr", 0, 24 + i, 1536, 1024, 768, 16, "bf16") for i in range(2)]
+    h = rl.Handle(0)
+    sets = []
+    for c in cs:
+        ops, d, shape, out = _setup(rl, c)
+        sets.append((c, ops, d, shape, out, torch.empty(rl.workspace_size(shape), dtype=torch.uint8, device="cuda"),
+                     torch.cuda.Stream()))
+    errors = []
+
+    def work(i, reps):
+        c, ops, d, shape, out, ws, st = sets[i]
+        try:
+            with torch.cuda.stream(st):
+                for _ in range(reps):
+                    h.forward(2 - i, shape, d["X"], d["W"], d["A"], d["B"], out["Y"], ws=ws)
+                    h.backward(1 + 4 * i, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], out["dX"], out["dA"],
+                               out["dB"], ws=ws)
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    ths = [threading.Thread(target=work, args=(i, 50)) for i in range(2)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errors, errors
+    got = [{k: v.clone() for k, v in s[4].items()} for s in sets]
+    for i, (c, ops, d, shape, out, ws, st) in enumerate(sets):
+        Xn, Wn, An, Bn, dYn = (_np(ops[k]) for k in ("X", "W", "A", "B", "dY"))
+        wA, wB, wX = O.reference_backward(Xn, Wn, An, Bn, dYn)
+        assert O.rel_fro(_np(out["Y"]), O.forward(1, Xn, Wn, An, Bn)) <= TOL
+        assert O.rel_fro(_np(out["dX"]), wX) <= TOL
+        assert O.rel_fro(_np(out["dA"]), wA) <= TOL
+        assert O.rel_fro(_np(out["dB"]), wB) <= TOL
+        work(i, 1)  # single-threaded rerun: bit-identical
+    torch.cuda.synchronize()
+    for i in range(2):
+        for k in ("Y", "dX", "dA", "dB"):
+            assert torch.equal(got[i][k], sets[i][4][k]), (i, k)
+
+
+def test_step_host_exchange_hook(rl):
+    """runlora_step_host calls the exchange hook after the backward and before the D2H copies:
+    a hook that doubles dA, dB on the stream must be seen in the host buffers."""
+    c = synth.case("e2ex", 0, 26, 640, 512, 768, 16, "bf16")
+    ops, d, shape, out = _setup(rl, c)
+    h = rl.handle(0)
+    host = {"X": ops["X"].pin_memory(), "dY": ops["dY"].pin_memory(),
+            "dA": torch.empty(c.k, c.r).pin_memory(), "dB": torch.empty(c.r, c.m).pin_memory(),
+            "dX": torch.empty(c.n, c.k, dtype=torch.bfloat16).pin_memory()}
+    dev = {"W": d["W"], "A": d["A"], "B": d["B"], "X": torch.empty_like(d["X"]), "dY": torch.empty_like(d["dY"]),
+           **out}
+    calls = []
+
+    def hook():
+        calls.append(1)
+        out["dA"].mul_(2.0)
+        out["dB"].mul_(2.0)
+
+    h.step_host(shape, 2, 5, host, dev, rl.F32, exchange=hook)
+    torch.cuda.synchronize()
+    assert calls == [1]
+    Xn, Wn, An, Bn, dYn = (_np(ops[k]) for k in ("X", "W", "A", "B", "dY"))
+    wA, wB, wX = O.reference_backward(Xn, Wn, An, Bn, dYn)
+    assert O.rel_fro(host["dA"].double().numpy(), 2 * wA) <= TOL
+    assert O.rel_fro(host["dB"].double().numpy(), 2 * wB) <= TOL
+    assert O.rel_fro(_np(host["dX"]), wX) <= TOL

@@ -97,24 +97,35 @@ torch.save({{"Y": Y.cpu(), "dX": dX.cpu(), "dA": dA.cpu(), "dB": dB.cpu()}}, sys
 
 
 def test_wide_reduced_stages_bit_exact(tmp_path):
-    """RUNLORA_MAIN_STAGES < 7 (set by bench.py under data parallelism) runs the 512-wide
-    kernel on 3 of its 4 ring stages: same arithmetic, so bit-identical outputs."""
+    """RUNLORA_MAIN_STAGES < 7 (set by bench.py under data parallelism) applies to the dX GEMM
+    only — the one the adapter-gradient allreduce overlaps: its 512-wide launch runs on 3 of
+    the 4 ring stages (48 KB less shared memory, RUNLORA_DEBUG_LAUNCH), the Y GEMM keeps the
+    full ring, and the arithmetic is unchanged, so every output is bit-identical."""
     import os
+    import re
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     script = tmp_path / "child.py"
     script.write_text(_CHILD.format(root=root))
-    outs = []
+    outs, smem = [], []
     for st in ("", "6"):
         env = dict(os.environ)
         env.pop("RUNLORA_MAIN_STAGES", None)
+        env["RUNLORA_DEBUG_LAUNCH"] = "1"
         if st:
             env["RUNLORA_MAIN_STAGES"] = st
         f = tmp_path / f"out{st or 'default'}.pt"
         p = subprocess.run([sys.executable, str(script), str(f)], env=env, capture_output=True, text=True, timeout=300)
         assert p.returncode == 0, p.stderr[-2000:]
         outs.append(torch.load(f))
+        # the two 512-wide main-GEMM launches of the child, in order: Y (forward), dX (backward)
+        wide = [int(m.group(1)) for m in re.finditer(r"tc_gemm<512,2,[^>]*> grid \d+ smem (\d+)", p.stderr)]
+        assert len(wide) == 2, p.stderr[-2000:]
+        smem.append(wide)
+    assert smem[0][0] == smem[0][1]                      # default: both on the full ring
+    assert smem[1][0] == smem[0][0]                      # reduced: the Y GEMM keeps it
+    assert smem[0][1] - smem[1][1] == 48 * 1024          # the dX GEMM drops one 48 KB stage
     for k in ("Y", "dX", "dA", "dB"):
         assert torch.equal(outs[0][k], outs[1][k]), k
 
