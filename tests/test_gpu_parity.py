@@ -223,3 +223,24 @@ def test_baseline_configs_c2_c3(rl, c):
 @pytest.mark.parametrize("c", list(synth.C4.values()), ids=lambda c: c.name)
 def test_baseline_configs_c4(rl, c):
     _sampled_check(rl, c, P=8)
+
+
+# ------------------------------------------- C4 per-rank shapes under token sharding
+# The exact shapes rank p runs at P = 8 (and 2, 4) ranks: n/P rows of C4; at
+# these sizes the selector flips to F1+B1 and the main GEMMs take the split-K path.
+PER_RANK_FULL = [synth.case(f"C4_rank_n{n}_r{r}", 4, 100 + 3 * j + i, n, 2048, 2048, r, "bf16")
+                 for j, n in enumerate((512, 1024, 2048)) for i, r in enumerate((8, 32, 128))]
+PER_RANK_SAMPLED = [synth.case(f"C4_rank_n{n}_r{r}", 4, 120 + 3 * j + i, n, 2048, 2048, r, "bf16")
+                    for j, n in enumerate((4096, 16384)) for i, r in enumerate((8, 32, 128))]
+
+
+@pytest.mark.parametrize("c", PER_RANK_FULL, ids=lambda c: c.name)
+def test_c4_per_rank_shapes_full(rl, c):
+    ops = synth.operands(c)
+    errs = _check_full(c, ops, _run_all(rl, c, _dev(ops)), TOL["bf16"])
+    assert max(errs.values()) < 5e-3, errs
+
+
+@pytest.mark.parametrize("c", PER_RANK_SAMPLED, ids=lambda c: c.name)
+def test_c4_per_rank_shapes_sampled(rl, c):
+    _sampled_check(rl, c)
