@@ -25,7 +25,6 @@ enum KernelId : int {
   KID_GEMM_SMALL,      // Z2'·Bᵀ, Z2'ᵀ·A (backward3/4 adapter grads)
   KID_SPLITK_REDUCE,   // fixed-order split-K reduction / cast / transpose
   KID_SGEMM_F32,       // fp32 SIMT GEMM (RUNLORA_F32 path)
-  KID_REPEAT_COLS,     // A repeated along its columns (dX tail against Z1's partial blocks)
   KID_QUANT,           // W -> FP8 E4M3 + per-column scales (column max, quantize, finalize)
   KID_DEQUANT,         // FP8 E4M3 W -> bf16 W in the workspace (QLoRA-style entry points)
   KID_ALLREDUCE,       // one-shot fixed-order allreduce of [dA | dB] over peer pointers
@@ -65,6 +64,17 @@ struct GemmReq {
   bool tma_store;  // OUT_BF16 through the TMA-store epilogue (all problems of a launch alike)
   bool overlaps_comm;  // the dX GEMM, which a data-parallel allreduce overlaps: runs on
                        // RUNLORA_MAIN_STAGES (fewer ring stages leave shared memory for NCCL)
+  int tail_rep, tail_w;  // repeated concat-K tail (Prob::tail_rep): K2 = tail_w, tail_rep blocks
+  // in-kernel split-K fix-up (Prob::fixup): the last split of each output tile reduces the
+  // slabs into fx_out (the ReduceJob semantics); counters zeroed by an earlier launch
+  bool fixup;
+  int* counters;
+  void* fx_out;
+  int64_t fx_ldo;
+  int fx_cols;
+  bool fx_transpose, fx_accumulate, fx_bf16;
+  int* zero_ptr;  // launch-level (first request): ints zeroed by CTA 0 after the PDL wait
+  int zero_n;
 };
 
 struct ReduceJob {
@@ -88,8 +98,6 @@ class Ctx {
   int main_cg() const { return main_cg_; }  // CTA-group size of the Y / dX GEMMs (env RUNLORA_MAIN_CG)
   bool occ2() const { return occ2_; }  // 2 CTAs/SM for rank-r kernels (env RUNLORA_OCC2=0 disables)
   bool pdl() const { return pdl_; }    // programmatic dependent launch (env RUNLORA_PDL=0 disables)
-  // split-K reductions of a backward whose launch waits until after its dX GEMM (same stream)
-  std::vector<ReduceJob> deferred_reduce;
   // 128x128 bf16 identity (device): A operand of the block-diagonal tail that adds W in W + A·B
   const void* identity() const { return identity_; }
   // debug timeline buffer (env RUNLORA_TRACE=<kernel id>): see GemmArgs::trace
@@ -136,8 +144,8 @@ class Ctx {
 
   std::mutex plan_mu;
   std::map<std::vector<int64_t>, runlora_plan_t> plans;
-  // Serialises every ABI call that enqueues work or touches the caches below (deferred
-  // reducer jobs, wide-tile plans, launch-trace slots, profiling events): any host thread
+  // Serialises every ABI call that enqueues work or touches the caches below (wide-tile
+  // plans, launch-trace slots, profiling events): any host thread
   // may call into a handle (e.g. autograd runs the backward on its own thread).  Recursive:
   // time-mode selection and runlora_step_host call the forward/backward entry points.
   std::recursive_mutex call_mu;
@@ -207,8 +215,6 @@ cudaError_t launch_allreduce_sum_f32(Ctx& ctx, const float* const* peers, int P,
                                      cudaStream_t s);
 cudaError_t launch_dequantize_w(Ctx& ctx, const void* Wq, const float* scale, int64_t k, int64_t m, void* W,
                                 cudaStream_t s);
-// dst[i, t*cols + j] = src[i, j] for t < reps (bf16, row-major; 16-byte column groups).
-cudaError_t launch_repeat_cols(Ctx& ctx, const void* src, int rows, int cols, int reps, void* dst, cudaStream_t s);
 // fp32 SIMT GEMM: C[i,j] = (acc ? C[i,j] : 0) + (Cadd ? Cadd[i,j] : 0) + sum_t A(i,t) B(t,j),
 // A(i,t) = A[i*sa0 + t*sa1], B(t,j) = B[t*sb0 + j*sb1].
 cudaError_t launch_sgemm(Ctx& ctx, int M, int N, int K, const float* A, int64_t sa0, int64_t sa1, const float* B,

@@ -15,7 +15,7 @@ namespace runlora {
 
 const char* const kKernelNames[KID_COUNT] = {
     "gemm_main",      "gemm_wprime", "gemm_proj",        "gemm_tokred",
-    "gemm_dense_xtdy", "gemm_small",  "splitk_reduce", "sgemm_f32", "repeat_cols", "quantize_w", "dequantize_w",
+    "gemm_dense_xtdy", "gemm_small",  "splitk_reduce", "sgemm_f32", "quantize_w", "dequantize_w",
     "allreduce_sum",
 };
 
@@ -192,23 +192,6 @@ __global__ void __launch_bounds__(256, 4) splitk_reduce_kernel(const __grid_cons
   if (threadIdx.x == 0) ltrace_mark(a.ltrace, 2);
 }
 
-// ------------------------------------------------------------ column repeat
-__global__ void __launch_bounds__(256) repeat_cols_kernel(const uint4* __restrict__ src, int rows, int g, int reps,
-                                                          uint4* __restrict__ dst, unsigned long long* lt) {
-  if (threadIdx.x == 0) ltrace_mark(lt, 0);
-  pdl_wait();
-  pdl_launch_dependents();
-  if (threadIdx.x == 0) ltrace_mark(lt, 1);
-  const long long total = (long long)rows * g * reps;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long i = idx / ((long long)g * reps);
-    const int c = (int)(idx % g);
-    dst[idx] = src[i * g + c];
-  }
-  if (threadIdx.x == 0) ltrace_mark(lt, 2);
-}
-
 // ------------------------------------------------------------ fp32 SIMT GEMM
 // 64x64 output tile per 256-thread CTA, 4x4 per thread, K step 16; true FP32 FFMA.
 __global__ void __launch_bounds__(256) sgemm_kernel(int M, int N, int K, const float* __restrict__ A, long long sa0,
@@ -362,6 +345,30 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
       return cudaErrorInvalidValue;
     }
     p.tail_diag = r.tail_diag ? 1 : 0;
+    if (r.tail_rep > 0) {
+      if (r.K2 != r.tail_w || r.tail_w <= 0 || r.tail_w > kBK || r.tail_diag) {
+        if (err) *err = "tc_gemm: a repeated tail needs K2 == tail_w <= 64";
+        return cudaErrorInvalidValue;
+      }
+      p.tail_rep = r.tail_rep;
+      p.tail_w = r.tail_w;
+      p.nk2 = r.tail_rep;
+    }
+    if (r.fixup) {
+      if (!(r.out_mode == OUT_F32 || r.out_mode == OUT_F32_FOLD) || cg != 1 || !r.counters || !r.fx_out ||
+          r.ldd % 4 != 0) {
+        if (err) *err = "tc_gemm: the split fix-up needs an fp32 slab output, single-CTA tiles and counters";
+        return cudaErrorInvalidValue;
+      }
+      p.fixup = 1;
+      p.counters = r.counters;
+      p.fx_out = r.fx_out;
+      p.fx_ldo = r.fx_ldo;
+      p.fx_cols = r.fx_cols;
+      p.fx_transpose = r.fx_transpose;
+      p.fx_accumulate = r.fx_accumulate;
+      p.fx_bf16 = r.fx_bf16;
+    }
     p.hint_a = r.a_policy == 1 ? kEvictNormal : r.a_policy == 2 ? kEvictFirst
                : r.a_stream_once ? kEvictFirst : kEvictNormal;
     p.hint_b = kEvictLast;
@@ -369,6 +376,8 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
     if (r.BN > bn_max) bn_max = r.BN;
   }
   g.nprob = nreq;
+  g.zero_ptr = reqs[0].zero_ptr;
+  g.zero_n = reqs[0].zero_ptr ? reqs[0].zero_n : 0;
   g.trace = (ctx.trace && ctx.trace_kid == reqs[0].kid && g.total_units <= Ctx::kTraceUnits) ? ctx.trace : nullptr;
   g.ltrace = ctx.ltrace_slot(reqs[0].kid);
   g.stages = (reqs[0].kid == KID_GEMM_MAIN && reqs[0].overlaps_comm) ? ctx.main_stages() : 0;
@@ -406,20 +415,6 @@ cudaError_t launch_splitk_reduce(Ctx& ctx, const ReduceJob* jobs, int njobs, cud
   a.ltrace = ctx.ltrace_slot(KID_SPLITK_REDUCE);
   ctx.launch_begin(s, KID_SPLITK_REDUCE);
   cudaError_t e = launch_pdl(ctx, splitk_reduce_kernel, dim3((unsigned)blocks), dim3(256), s, a);
-  ctx.launch_end(s);
-  return e;
-}
-
-cudaError_t launch_repeat_cols(Ctx& ctx, const void* src, int rows, int cols, int reps, void* dst, cudaStream_t s) {
-  if (cols % 8 != 0) return cudaErrorInvalidValue;  // 16-byte groups of bf16
-  const int g = cols / 8;
-  const long long total = (long long)rows * g * reps;
-  long long blocks = (total + 255) / 256;
-  if (blocks > ctx.num_sms() * 8LL) blocks = ctx.num_sms() * 8LL;
-  ctx.launch_begin(s, KID_REPEAT_COLS);
-  cudaError_t e = launch_pdl(ctx, repeat_cols_kernel, dim3((unsigned)blocks), dim3(256), s,
-                             static_cast<const uint4*>(src), rows, g, reps, static_cast<uint4*>(dst),
-                             ctx.ltrace_slot(KID_REPEAT_COLS));
   ctx.launch_end(s);
   return e;
 }

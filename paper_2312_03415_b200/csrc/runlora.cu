@@ -214,15 +214,16 @@ GemmReq base_req(int M, int N, KernelId kid) {
   return q;
 }
 
-// defer_reduce: the reducer is not launched here but stashed in the context; the caller
-// (do_backward) launches it on the same stream right after the dX GEMM, where it
-// co-resides with that GEMM's tail in the programmatic-dependent-launch chain (a side
-// stream joined by events breaks the chain: measured 5-7 µs per event wait).
-runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, KernelId kid, cudaStream_t st,
-                            bool defer_reduce = false) {
+// Split (!direct) plans reduce their fp32 slabs inside the same launch: the last split of
+// each output tile to finish sums the slabs in split order (Prob::fixup, deterministic).
+// The fix-up counters (per output tile) are zeroed by a memset node ahead of the launch —
+// this path serves shapes off the hot configurations (small n, backward2..4); the backward1/5
+// hot path zeroes them inside its projection launch instead (grads_tok_bf16).
+runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, int* counters, KernelId kid,
+                            cudaStream_t st) {
   const SkinnyPlan p = plan_skinny(jobs, n);
   GemmReq q[2];
-  ReduceJob rj[2];
+  int ntiles = 0;
   for (int i = 0; i < n; ++i) {
     const Skinny& j = jobs[i];
     q[i] = base_req((int)j.rows, p.direct ? (int)j.r : p.Npad[i], kid);
@@ -245,21 +246,24 @@ runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, KernelI
       q[i].split_stride = j.rows * (int64_t)p.Npad[i];
       q[i].splits = p.splits[i];
       q[i].kb_per_split = p.kps[i];
+      q[i].fixup = true;
+      q[i].counters = counters + ntiles;
+      q[i].fx_out = j.out;
+      q[i].fx_ldo = j.ldo;
+      q[i].fx_cols = (int)j.r;
+      q[i].fx_transpose = j.transpose;
+      q[i].fx_accumulate = j.accumulate;
+      q[i].fx_bf16 = j.out_bf16;
+      ntiles += (int)(((j.rows + kBM - 1) / kBM) * (p.Npad[i] / p.BN[i]));
     }
-    rj[i] = ReduceJob{Pi, p.splits[i], j.rows * (int64_t)p.Npad[i], (int)j.rows, (int)j.r, p.Npad[i], j.out,
-                      j.out_bf16 ? 1 : 0, j.ldo, j.transpose ? 1 : 0, j.accumulate ? 1 : 0};
+  }
+  if (!p.direct) {
+    cudaError_t e = cudaMemsetAsync(counters, 0, sizeof(int) * (size_t)ntiles, st);
+    if (e != cudaSuccess) return cuda_fail(e, "fix-up counter reset");
   }
   std::string err;
   cudaError_t e = launch_tc_gemm(c, q, n, st, &err);
   if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
-  if (!p.direct) {
-    if (defer_reduce) {
-      c.deferred_reduce.assign(rj, rj + n);
-      return RUNLORA_OK;
-    }
-    e = launch_splitk_reduce(c, rj, n, st);
-    if (e != cudaSuccess) return cuda_fail(e, "splitk_reduce launch");
-  }
   return RUNLORA_OK;
 }
 
@@ -416,12 +420,16 @@ size_t main_split_bytes(const runlora_shape_t& s) {
 }
 
 struct Layout {
-  size_t z1, z2, arep, brep, wp, p, pm, total;
+  size_t z1, z2, cnt, wp, p, pm, total;
 };
 
-// Z1, Z2: n x r (or n x sz*r partial blocks, see ZPlan); arep: A repeated sz times along its
-// columns (k x sz*r, backward1's dX tail against Z1's blocks); brep: B stacked sz times
-// (sz*r x m, forward1's Y tail against Z2's blocks).
+// Split fix-up counters: one int per output tile of a split rank-r launch (both problems).
+size_t counter_count(const runlora_shape_t& s) {
+  const int64_t rows = std::max({s.n, s.k, s.m});
+  return (size_t)(2 * ((rows + kBM - 1) / kBM) * ((s.r + 15) / 16) + 64);
+}
+
+// Z1, Z2: n x r (or n x sz*r partial blocks, see ZPlan); cnt: split fix-up counters.
 Layout layout_of(const runlora_shape_t& s) {
   const size_t es = s.dtype == RUNLORA_BF16 ? 2 : 4;
   const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
@@ -431,9 +439,8 @@ Layout layout_of(const runlora_shape_t& s) {
   Layout L;
   L.z1 = 0;
   L.z2 = al((size_t)n * zc * es);
-  L.arep = L.z2 + al((size_t)n * zc2 * es);
-  L.brep = L.arep + (f.ok && f.sz > 1 ? al((size_t)k * zc * es) : 0);
-  L.wp = L.brep + (f.ok && f.szf > 1 ? al((size_t)m * r * f.szf * es) : 0);
+  L.cnt = L.z2 + al((size_t)n * zc2 * es);
+  L.wp = L.cnt + al(4 * counter_count(s));
   L.p = L.wp + al((size_t)k * m * es);
   L.pm = L.p + (s.dtype == RUNLORA_BF16 ? partial_need(s) : 0);  // main-GEMM split-K slabs after
   L.total = L.pm + (s.dtype == RUNLORA_BF16 ? main_split_bytes(s) : 0);  // the rank-r ones (see main_gemm)
@@ -441,8 +448,9 @@ Layout layout_of(const runlora_shape_t& s) {
 }
 
 struct Bufs {
-  void *z1, *z2, *arep, *brep, *wp;
-  float* P;   // rank-r split-K slabs (may still await the deferred reducer during the dX GEMM)
+  void *z1, *z2, *wp;
+  int* cnt;   // split fix-up counters
+  float* P;   // rank-r split-K slabs
   float* Pm;  // main-GEMM split-K slabs
 };
 
@@ -458,8 +466,7 @@ runlora_status_t bind_ws(const runlora_shape_t& s, void* ws, size_t ws_bytes, Bu
   char* base = static_cast<char*>(ws);
   b->z1 = base + L.z1;
   b->z2 = base + L.z2;
-  b->arep = base + L.arep;
-  b->brep = base + L.brep;
+  b->cnt = reinterpret_cast<int*>(base + L.cnt);
   b->wp = base + L.wp;
   b->P = reinterpret_cast<float*>(base + L.p);
   b->Pm = reinterpret_cast<float*>(base + L.pm);
@@ -676,10 +683,9 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
     const ZPlan f = plan_z(s);
     if (f.ok && f.szf > 1) {
       // Z2 as szf K-split bf16 blocks (every CTA slot streams X, no reducer), then
-      // Y = [X | Z2_0 | .. | Z2_{szf-1}]·[W ; B ; .. ; B] (B stacked szf times, side stream)
+      // Y = [X | Z2_0 | .. | Z2_{szf-1}]·[W ; B ; .. ; B]: the tail repeats B itself per block
+      // (Prob::tail_rep), no stacked copy of B
       const int zc = (int)(r * f.szf);
-      cudaError_t e = launch_repeat_cols(c, B, 1, (int)(r * m), f.szf, b.brep, st);
-      if (e != cudaSuccess) return cuda_fail(e, "repeat_cols launch");
       GemmReq z = base_req((int)n, (int)r, KID_GEMM_PROJ);
       z.a = mat(X, n, k);
       z.b = mat(A, k, r);
@@ -695,11 +701,13 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
       z.kb_per_split = f.kpzf;
       RL_TRY(gemm(c, z, st));
       q.a2 = mat(b.z2, n, zc);
-      q.b2 = mat(b.brep, zc, m);
-      q.K2 = zc;
+      q.b2 = mat(B, r, m);
+      q.K2 = (int)r;
+      q.tail_rep = f.szf;
+      q.tail_w = (int)r;
     } else {
       Skinny j = job_Z2(s, X, A, b.z2);
-      RL_TRY(run_skinny(c, &j, 1, b.P, KID_GEMM_PROJ, st));
+      RL_TRY(run_skinny(c, &j, 1, b.P, b.cnt, KID_GEMM_PROJ, st));
       q.a2 = mat(b.z2, n, r);
       q.b2 = mat(B, r, m);
       q.K2 = (int)r;
@@ -712,19 +720,17 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
   return main_gemm(c, q, b, st);
 }
 
-// backward1/5 adapter gradients: projections launch, reductions launch, reducer (see ZPlan).
-runlora_status_t grads_tok_bf16(Ctx& c, int v, const ZPlan& f, const runlora_shape_t& s, const void* X,
-                                const void* A, const void* B, const void* dY, void* dA, void* dB, bool gb, bool acc,
-                                Bufs& b, cudaStream_t st, bool defer) {
+// backward1/5 adapter gradients: projections launch, then reductions launch whose last split
+// per output tile sums the token-split slabs in fixed order (see ZPlan; no reducer launch).
+runlora_status_t grads_tok_bf16(Ctx& c, const ZPlan& f, const runlora_shape_t& s, const void* X, const void* A,
+                                const void* B, const void* dY, void* dA, void* dB, bool gb, bool acc, Bufs& b,
+                                cudaStream_t st) {
   const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
   const int zc = (int)(r * f.sz);  // columns of the partial-Z matrices
+  const int tiles[2] = {(int)((k + kBM - 1) / kBM), (int)((m + kBM - 1) / kBM)};  // reduction output tiles
   std::string err;
-  if (v == 1 && f.sz > 1) {
-    // A repeated sz times for backward1's dX tail (2 µs; in the same PDL chain)
-    cudaError_t e = launch_repeat_cols(c, A, (int)k, (int)r, f.sz, b.arep, st);
-    if (e != cudaSuccess) return cuda_fail(e, "repeat_cols launch");
-  }
-  // projections: Zp[:, s*r:(s+1)*r] = K-split s of dY·Bᵀ / X·A (bf16)
+  // projections: Zp[:, s*r:(s+1)*r] = K-split s of dY·Bᵀ / X·A (bf16); this launch also zeroes
+  // the reductions' fix-up counters (after its PDL wait, so no earlier launch still uses them)
   GemmReq q[2];
   const DeviceMat za[2] = {mat(dY, n, m), mat(X, n, k)};
   const DeviceMat zb[2] = {mat(B, r, m), mat(A, k, r)};
@@ -745,10 +751,12 @@ runlora_status_t grads_tok_bf16(Ctx& c, int v, const ZPlan& f, const runlora_sha
     g.splits = f.sz;
     g.kb_per_split = f.kpz[i];
   }
+  q[0].zero_ptr = b.cnt;
+  q[0].zero_n = tiles[0] + tiles[1];
   cudaError_t e = launch_tc_gemm(c, q, 2, st, &err);
   if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
-  // reductions: dA = Σ_s Xᵀ·Z1_s, dBᵀ = Σ_s dYᵀ·Z2_s (token splits -> fp32 slabs)
-  ReduceJob rj[2];
+  // reductions: dA = Σ_s Xᵀ·Z1_s, dBᵀ = Σ_s dYᵀ·Z2_s (token splits -> fp32 slabs, fixed-order
+  // in-kernel fix-up into dA [k, r] and dB [r, m] (transposed), fp32 or bf16, = or +=)
   const DeviceMat ta[2] = {mat(X, n, k), mat(dY, n, m)};
   const int64_t rows[2] = {k, m};
   void* outs[2] = {dA, dB};
@@ -776,35 +784,34 @@ runlora_status_t grads_tok_bf16(Ctx& c, int v, const ZPlan& f, const runlora_sha
       g.ldd = f.bn_t;  // plain slabs keep the padded tile width
     }
     g.split_stride = rows[i] * g.ldd;
-    rj[i] = ReduceJob{P, f.tsplits, g.split_stride, (int)rows[i], (int)r, g.ldd, outs[i], gb ? 1 : 0,
-                      i == 0 ? r : m, i == 1 ? 1 : 0, acc ? 1 : 0};
+    g.fixup = true;
+    g.counters = b.cnt + (i == 0 ? 0 : tiles[0]);
+    g.fx_out = outs[i];
+    g.fx_ldo = i == 0 ? r : m;
+    g.fx_cols = (int)r;
+    g.fx_transpose = i == 1;
+    g.fx_accumulate = acc;
+    g.fx_bf16 = gb;
   }
   e = launch_tc_gemm(c, q, 2, st, &err);
   if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
-  if (defer) {  // launched by do_backward right after the dX GEMM
-    c.deferred_reduce.assign(rj, rj + 2);
-    return RUNLORA_OK;
-  }
-  e = launch_splitk_reduce(c, rj, 2, st);
-  if (e != cudaSuccess) return cuda_fail(e, "splitk_reduce launch");
   return RUNLORA_OK;
 }
 
 runlora_status_t params_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* X, const void* A, const void* B,
-                             const void* dY, void* dA, void* dB, bool gb, bool acc, Bufs& b, cudaStream_t st,
-                             bool defer = false) {
+                             const void* dY, void* dA, void* dB, bool gb, bool acc, Bufs& b, cudaStream_t st) {
   const int64_t n = s.n, k = s.k, m = s.m;
   if (v == 1 || v == 5) {  // Alg. 1 / Alg. 5: Z1, Z2 | dA = Xᵀ·Z1, dB = Z2ᵀ·dY
     const ZPlan f = plan_z(s);
-    if (f.ok) return grads_tok_bf16(c, v, f, s, X, A, B, dY, dA, dB, gb, acc, b, st, defer);
+    if (f.ok) return grads_tok_bf16(c, f, s, X, A, B, dY, dA, dB, gb, acc, b, st);
     Skinny pj[2] = {job_Z1(s, dY, B, b.z1), job_Z2(s, X, A, b.z2)};
-    RL_TRY(run_skinny(c, pj, 2, b.P, KID_GEMM_PROJ, st));
+    RL_TRY(run_skinny(c, pj, 2, b.P, b.cnt, KID_GEMM_PROJ, st));
     Skinny tj[2] = {job_dA_tok(s, X, b.z1, dA, gb, acc), job_dB_tok(s, dY, b.z2, dB, gb, acc)};
-    return run_skinny(c, tj, 2, b.P, KID_GEMM_TOKRED, st, defer);
+    return run_skinny(c, tj, 2, b.P, b.cnt, KID_GEMM_TOKRED, st);
   }
   if (v == 2 || v == 3) {  // Z1 = dY·Bᵀ
     Skinny j = job_Z1(s, dY, B, b.z1);
-    RL_TRY(run_skinny(c, &j, 1, b.P, KID_GEMM_PROJ, st));
+    RL_TRY(run_skinny(c, &j, 1, b.P, b.cnt, KID_GEMM_PROJ, st));
   }
   {  // Z2' = Xᵀ·dY (k×m): A_op = Xᵀ (MN-major X), B_op = dY (MN-major)
     GemmReq q = base_req((int)k, (int)m, KID_GEMM_DENSE_XTDY);
@@ -822,11 +829,11 @@ runlora_status_t params_bf16(Ctx& c, int v, const runlora_shape_t& s, const void
   }
   if (v == 2) {  // dA = Xᵀ·Z1, dB = Aᵀ·Z2'
     Skinny j[2] = {job_dA_tok(s, X, b.z1, dA, gb, acc), job_dB_dense(s, b.wp, A, dB, gb, acc)};
-    return run_skinny(c, j, 2, b.P, KID_GEMM_SMALL, st, defer);
+    return run_skinny(c, j, 2, b.P, b.cnt, KID_GEMM_SMALL, st);
   }
   // v = 3, 4: dA = Z2'·Bᵀ, dB = Aᵀ·Z2'
   Skinny j[2] = {job_dA_dense(s, b.wp, B, dA, gb, acc), job_dB_dense(s, b.wp, A, dB, gb, acc)};
-  return run_skinny(c, j, 2, b.P, KID_GEMM_SMALL, st, defer);  // the reducer reads only the slabs
+  return run_skinny(c, j, 2, b.P, b.cnt, KID_GEMM_SMALL, st);
 }
 
 runlora_status_t input_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* W, const void* A, const void* B,
@@ -848,11 +855,11 @@ runlora_status_t input_bf16(Ctx& c, int v, const runlora_shape_t& s, const void*
     const ZPlan f = plan_z(s);
     if (v == 1 && f.ok && f.sz > 1) {
       // backward1's adapter-gradient pass left Z1 as sz partial blocks: dY·Wᵀ + Σ_s Z1_s·Aᵀ =
-      // [dY | Z1_0 | .. | Z1_{sz-1}]·[Wᵀ ; Aᵀ ; .. ; Aᵀ]
-      const int zc = (int)(r * f.sz);
-      q.a2 = mat(b.z1, n, zc);
-      q.b2 = mat(b.arep, k, zc);
-      q.K2 = zc;
+      // [dY | Z1_0 | .. | Z1_{sz-1}]·[Wᵀ ; Aᵀ ; .. ; Aᵀ], the tail repeating A itself per
+      // block (Prob::tail_rep)
+      q.a2 = mat(b.z1, n, (int64_t)r * f.sz);
+      q.tail_rep = f.sz;
+      q.tail_w = (int)r;
     }
   } else {  // dX = dY·W'ᵀ
     RL_TRY(wprime_bf16(c, s, W, A, B, b.wp, st));
@@ -991,7 +998,7 @@ runlora_status_t validate_input(runlora_handle_t h, int bwd, const runlora_shape
 
 runlora_status_t do_params(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X, const void* W,
                            const void* A, const void* B, const void* dY, void* dA, void* dB, int grad_dtype,
-                           int accumulate, void* ws, size_t ws_bytes, void* stream, bool defer = false) {
+                           int accumulate, void* ws, size_t ws_bytes, void* stream) {
   (void)W;
   RL_TRY(validate_params(h, bwd, s, X, A, B, dY, dA, dB, grad_dtype));
   Bufs b;
@@ -1000,8 +1007,7 @@ runlora_status_t do_params(runlora_handle_t h, int bwd, const runlora_shape_t* s
   DeviceGuard dg(h->ctx->device());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (s->dtype == RUNLORA_BF16)
-    RL_TRY(params_bf16(*h->ctx, bwd, *s, X, A, B, dY, dA, dB, grad_dtype == RUNLORA_BF16, accumulate != 0, b, st,
-                       defer));
+    RL_TRY(params_bf16(*h->ctx, bwd, *s, X, A, B, dY, dA, dB, grad_dtype == RUNLORA_BF16, accumulate != 0, b, st));
   else
     RL_TRY(params_f32(*h->ctx, bwd, *s, X, A, B, dY, dA, dB, accumulate != 0, b, st));
   return post_launch();
@@ -1031,23 +1037,10 @@ runlora_status_t do_backward(runlora_handle_t h, int bwd, const runlora_shape_t*
     RL_TRY(bind_ws(*s, ws, ws_bytes, &b));
   }
   CallLock lk(h->ctx->call_mu);
-  // With dX, the adapter-gradient reducer is launched after the dX GEMM on the same stream:
-  // it co-resides with the GEMM's last wave and the whole backward stays one
-  // programmatic-dependent-launch chain (no cross-stream events).
-  const bool defer = dX != nullptr;
-  h->ctx->deferred_reduce.clear();
-  runlora_status_t st = do_params(h, bwd, s, X, W, A, B, dY, dA, dB, grad_dtype, accumulate, ws, ws_bytes, stream,
-                                  defer);
-  if (st == RUNLORA_OK && dX) st = do_input(h, bwd, s, W, A, B, dY, dX, ws, ws_bytes, stream);
-  if (!h->ctx->deferred_reduce.empty()) {
-    // launched even if dX failed, so dA/dB are complete whenever the call reports success
-    DeviceGuard dg(h->ctx->device());
-    cudaError_t e = launch_splitk_reduce(*h->ctx, h->ctx->deferred_reduce.data(),
-                                         (int)h->ctx->deferred_reduce.size(), static_cast<cudaStream_t>(stream));
-    h->ctx->deferred_reduce.clear();
-    if (e != cudaSuccess && st == RUNLORA_OK) st = cuda_fail(e, "splitk_reduce launch");
-  }
-  return st;
+  // adapter gradients (reduced inside their own launches), then dX — one PDL chain
+  RL_TRY(do_params(h, bwd, s, X, W, A, B, dY, dA, dB, grad_dtype, accumulate, ws, ws_bytes, stream));
+  if (dX) RL_TRY(do_input(h, bwd, s, W, A, B, dY, dX, ws, ws_bytes, stream));
+  return RUNLORA_OK;
 }
 
 // ------------------------------------------------------------ selector

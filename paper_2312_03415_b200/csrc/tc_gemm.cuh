@@ -74,6 +74,22 @@ struct Prob {
   // B2 that belong to this tile's own M range.  D += I·B2[m0.., n0..] adds a matrix that is
   // indexed like the output (W + A·B: the add rides in the mainloop, exact in fp32).
   int tail_diag;
+  // Repeated concat-K tail: nk2 = tail_rep k-blocks, block s multiplies columns
+  // [s*tail_w, (s+1)*tail_w) of A2 with columns [0, tail_w) of the SAME B2 (e.g. Σ_s Z1_s·Aᵀ
+  // over the K-split partial blocks of Z1 against A itself, no repeated copy of A).  The MMA
+  // issues ⌈tail_w/16⌉ K-steps; A2 columns past tail_w inside a step meet B2's zero-filled
+  // (out-of-bounds) K rows.  0 = a plain tail.
+  int tail_rep, tail_w;
+  // Split-K fix-up (fp32 slab modes): the last split of an output tile to finish sums the
+  // num_splits slabs of that tile in split order (deterministic) and writes
+  //   out[i, c] (or out[c, i] when fx_transpose) {=, +=} sum_s slab[s][i][c],  c < fx_cols,
+  // as fp32 or bf16.  counters: one int per output tile, zero before the launch (the
+  // launch that zeroes them is GemmArgs::zero_ptr of an earlier launch in the stream).
+  int fixup;
+  int* counters;
+  void* fx_out;
+  long long fx_ldo;
+  int fx_cols, fx_transpose, fx_accumulate, fx_bf16;
 };
 
 constexpr int kMaxProb = 2;  // problems per launch (dual launches); kernel params stay ~1.8 KB
@@ -91,6 +107,8 @@ struct GemmArgs {
   unsigned long long* trace;
   unsigned long long* ltrace;  // launch timeline slot (nullptr: off)
   int stages;                  // pipeline stages (0: the compiled maximum TileCfg::STAGES)
+  int* zero_ptr;               // zeroed by CTA 0 after the PDL wait (split fix-up counters of a
+  int zero_n;                  // later launch in the stream), nullptr: none
 };
 
 struct Tmaps {  // per problem: A1, B1, A2, B2, D (EPI = 3: TMA-store epilogue)
@@ -225,6 +243,40 @@ __device__ __forceinline__ void store_row_segment(const Prob& p, int split, int 
 }
 
 
+// Split-K fix-up of output tile (m_blk, n_blk) of problem p, run by the 4 epilogue warps of
+// the CTA whose split arrived last (Prob::fixup).  Thread = row; fixed split order.
+__device__ __forceinline__ void split_fixup(const Prob& p, int row, int n_blk) {
+  if (row >= p.M) return;
+  const int c_lo = n_blk * p.bn, c_hi = min(p.fx_cols, c_lo + p.bn);
+  const float* base = static_cast<const float*>(p.D) + (long long)row * p.ldd;
+  for (int c0 = c_lo; c0 < c_hi; c0 += 4) {
+    float4 acc = __ldcg(reinterpret_cast<const float4*>(base + c0));
+    for (int sp = 1; sp < p.num_splits; ++sp) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(base + sp * p.split_stride + c0));
+      acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+    }
+    const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int c = c0 + x;
+      if (c >= c_hi) break;
+      const long long o = p.fx_transpose ? (long long)c * p.fx_ldo + row : (long long)row * p.fx_ldo + c;
+      float v = a4[x];
+      if (p.fx_bf16) {
+        __nv_bfloat16* d = static_cast<__nv_bfloat16*>(p.fx_out) + o;
+        if (p.fx_accumulate) v += __bfloat162float(*d);
+        *d = __float2bfloat16_rn(v);
+      } else {
+        float* d = static_cast<float*>(p.fx_out) + o;
+        if (p.fx_accumulate) v += *d;
+        *d = v;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
 // EPI = 3: one 32-row x 64-column bf16 chunk of a warp (row = lane) -> its staging buffer
 // (128B swizzle: 16-byte chunk e of row r at (e ^ (r & 7)) * 16) -> TMA store.  A buffer is
 // reused only after the store issued NB chunks earlier has finished reading it.
@@ -306,6 +358,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  volatile int* fx_last = reinterpret_cast<volatile int*>(tmem_slot + 1);  // split fix-up: this CTA arrived last
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -342,6 +395,8 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
   // everything above overlapped the previous kernel's tail (PDL); inputs are read below
   pdl_wait();
   pdl_launch_dependents();
+  if (g.zero_ptr && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < g.zero_n; i += blockDim.x) g.zero_ptr[i] = 0;
   if (ctrace && threadIdx.x == 0) ctrace[1] = globaltimer();
   if (threadIdx.x == 0) ltrace_mark(g.ltrace, 1);
 
@@ -394,9 +449,12 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
             const CUtensorMap* ta = &tm.m[t.prob][tail ? 2 : 0];
             const CUtensorMap* tb = &tm.m[t.prob][tail ? 3 : 1];
             const int ki = rev ? nmain - 1 - i : i;
-            const int kc = (tail ? (i - nmain) : (kb0 + ki)) * kBK;
+            // K coordinates of the A and B boxes: main k-block, plain tail block, repeated
+            // tail block (A2 column block s against B2 from K = 0), identity tail (B2 rows of
+            // this tile)
+            const int kc = !tail ? (kb0 + ki) * kBK : p.tail_rep ? (i - nmain) * p.tail_w : (i - nmain) * kBK;
             const int ma = diag ? 0 : m0;          // identity tail: rows of I
-            const int kcb = diag ? m0 + kc : kc;   // identity tail: B2 rows of this tile
+            const int kcb = diag ? m0 + kc : (tail && p.tail_rep) ? 0 : kc;
             if (skip_a) {
             } else if (!p.a_mn) {
               tma_load_2d<CG>(ta, fb, a, kc, ma, p.hint_a);
@@ -468,7 +526,9 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
         for (int at = 0; at < natoms; ++at) {
           const int i = i0 + at;
           const int ki = rev ? nmain - 1 - i : i;
-          const int kleft = (i < nmain) ? (p.k1 - (kb0 + ki) * kBK) : (p.k2 - (i - nmain) * kBK);
+          const int kleft = (i < nmain)   ? (p.k1 - (kb0 + ki) * kBK)
+                            : p.tail_rep ? p.tail_w
+                                         : (p.k2 - (i - nmain) * kBK);
           const int ksteps = min(kBK / 16, (kleft + 15) >> 4);
           const uint32_t a_addr = smem_u32(sA + st * C::A_BYTES + at * C::A_ATOM);
           const uint32_t b_addr = smem_u32(sB + st * C::B_BYTES + at * C::B_ATOM);
@@ -703,6 +763,18 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
         else ++use0;
       }
       sc += nh;
+      if (p.fixup) {
+        // split-K fix-up: count this split's arrival at its output tile once all 128 rows of
+        // the slab are stored; the last split to arrive reduces the tile (Prob::fixup)
+        __threadfence();
+        epi_bar();
+        if (threadIdx.x == 4 * 32) *fx_last = atomicAdd(&p.counters[t.m_blk * p.num_n_tiles + t.n_blk], 1) == p.num_splits - 1;
+        epi_bar();
+        if (*fx_last) {
+          __threadfence();
+          split_fixup(p, row, t.n_blk);
+        }
+      }
       if (g.trace && threadIdx.x == 4 * 32) g.trace[8 * u + 3] = globaltimer();
     }
     if constexpr (EPI == 3) {
