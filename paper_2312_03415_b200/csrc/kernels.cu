@@ -388,12 +388,27 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
   if (const char* d = getenv("RUNLORA_DBG_GEMM")) g.dbg = atoi(d);
   for (int q = nreq; q < kMaxProb; ++q) g.p[q] = g.p[0], g.p[q].units = 0;
   if (g.total_units <= 0) return cudaSuccess;
+  // a CTA defers at most kMaxFixups split fix-ups to the end of its unit loop; beyond that
+  // (never on the shapes of the configs) the slabs are reduced by the reducer kernel instead
+  ReduceJob fallback[kMaxProb];
+  int nfb = 0;
+  const int min_groups = ctx.num_sms() / cg;
+  if ((g.total_units + min_groups - 1) / min_groups > kMaxFixups) {
+    for (int q = 0; q < nreq; ++q) {
+      Prob& p = g.p[q];
+      if (!p.fixup) continue;
+      p.fixup = 0;
+      fallback[nfb++] = ReduceJob{static_cast<const float*>(p.D), p.num_splits, p.split_stride, p.M, p.fx_cols, p.ldd,
+                                  p.fx_out, p.fx_bf16, p.fx_ldo, p.fx_transpose, p.fx_accumulate};
+    }
+  }
   ctx.launch_begin(s, reqs[0].kid);
   // 2 CTAs per SM for the HBM-bound rank-r kernels; at 128 columns only for the token
   // reductions (r = 128: 42.6 -> 31.0 µs; the projections lost 38 -> 45 µs to the shallower ring)
   const bool occ2 = ctx.occ2() && reqs[0].a_stream_once && (bn_max <= 64 || reqs[0].kid == KID_GEMM_TOKRED);
   cudaError_t e = dispatch_tc(ctx, bn_max, cg, occ2, tma_store, tm, g, s);
   ctx.launch_end(s);
+  if (e == cudaSuccess && nfb > 0) e = launch_splitk_reduce(ctx, fallback, nfb, s);
   if (e != cudaSuccess && err) *err = std::string("tc_gemm launch: ") + cudaGetErrorString(e);
   return e;
 }

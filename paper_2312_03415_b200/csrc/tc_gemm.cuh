@@ -117,6 +117,7 @@ struct Tmaps {  // per problem: A1, B1, A2, B2, D (EPI = 3: TMA-store epilogue)
 
 constexpr int kStgBufs = 4;  // EPI = 3 staging tiles per epilogue warp (a 256-wide tile's 4 stores never wait)
 constexpr int kBM = 128;  // rows per CTA
+constexpr int kMaxFixups = 64;  // split fix-ups one CTA can defer to the end of its unit loop
 constexpr int kBK = 64;
 constexpr int kGemmThreads = 256;
 
@@ -139,7 +140,8 @@ struct TileCfg {
   static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = (2 * BN_MAX <= 32) ? 32 : (2 * BN_MAX <= 64) ? 64
                                         : (2 * BN_MAX <= 128) ? 128 : (2 * BN_MAX <= 256) ? 256 : 512;
-  static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + STG_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + STG_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
+                                         4 * kMaxFixups /*split fix-up list*/;
 };
 
 struct Unit {
@@ -244,32 +246,48 @@ __device__ __forceinline__ void store_row_segment(const Prob& p, int split, int 
 
 
 // Split-K fix-up of output tile (m_blk, n_blk) of problem p, run by the 4 epilogue warps of
-// the CTA whose split arrived last (Prob::fixup).  Thread = row; fixed split order.
+// the CTA whose split arrived last (Prob::fixup), after its unit loop.  Thread = row; 16-column
+// chunks; the slabs are summed in split order (deterministic), two splits' loads (8 x 16 B)
+// in flight before any is added.
 __device__ __forceinline__ void split_fixup(const Prob& p, int row, int n_blk) {
   if (row >= p.M) return;
   const int c_lo = n_blk * p.bn, c_hi = min(p.fx_cols, c_lo + p.bn);
   const float* base = static_cast<const float*>(p.D) + (long long)row * p.ldd;
-  for (int c0 = c_lo; c0 < c_hi; c0 += 4) {
-    float4 acc = __ldcg(reinterpret_cast<const float4*>(base + c0));
-    for (int sp = 1; sp < p.num_splits; ++sp) {
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(base + sp * p.split_stride + c0));
-      acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
-    }
-    const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+  const long long ostep = p.fx_transpose ? p.fx_ldo : 1;
+  const long long obase = p.fx_transpose ? (long long)row : (long long)row * p.fx_ldo;
+  const int S = p.num_splits;
+#pragma unroll 1
+  for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
+    float a[16];
 #pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      const int c = c0 + x;
-      if (c >= c_hi) break;
-      const long long o = p.fx_transpose ? (long long)c * p.fx_ldo + row : (long long)row * p.fx_ldo + c;
-      float v = a4[x];
+    for (int e = 0; e < 16; ++e) a[e] = 0.f;
+#pragma unroll 1
+    for (int sp = 0; sp < S; sp += 2) {
+      float4 v[8];
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+        if (sp + (x >> 2) < S && c0 + 4 * (x & 3) < c_hi)
+          v[x] = __ldcg(reinterpret_cast<const float4*>(base + (sp + (x >> 2)) * p.split_stride + c0 + 4 * (x & 3)));
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+        if (sp + (x >> 2) < S && c0 + 4 * (x & 3) < c_hi) {
+          float* t = a + 4 * (x & 3);
+          t[0] += v[x].x, t[1] += v[x].y, t[2] += v[x].z, t[3] += v[x].w;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      if (c0 + e >= c_hi) break;
+      const long long o = obase + (long long)(c0 + e) * ostep;
+      float val = a[e];
       if (p.fx_bf16) {
         __nv_bfloat16* d = static_cast<__nv_bfloat16*>(p.fx_out) + o;
-        if (p.fx_accumulate) v += __bfloat162float(*d);
-        *d = __float2bfloat16_rn(v);
+        if (p.fx_accumulate) val += __bfloat162float(*d);
+        *d = __float2bfloat16_rn(val);
       } else {
         float* d = static_cast<float*>(p.fx_out) + o;
-        if (p.fx_accumulate) v += *d;
-        *d = v;
+        if (p.fx_accumulate) val += *d;
+        *d = val;
       }
     }
   }
@@ -358,7 +376,11 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  volatile int* fx_last = reinterpret_cast<volatile int*>(tmem_slot + 1);  // split fix-up: this CTA arrived last
+  // split fix-up: the tiles this CTA's splits completed last (packed prob|n_blk|m_blk), reduced
+  // after its unit loop, where the epilogue's registers are free (Prob::fixup)
+  volatile int* fx_count = reinterpret_cast<volatile int*>(tmem_slot + 1);
+  int* fx_list = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(full) + 256);
+  if (threadIdx.x == 4 * 32) *fx_count = 0;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -765,21 +787,31 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       sc += nh;
       if (p.fixup) {
         // split-K fix-up: count this split's arrival at its output tile once all 128 rows of
-        // the slab are stored; the last split to arrive reduces the tile (Prob::fixup)
+        // the slab are stored; the last split to arrive reduces the tile (after the loop)
         __threadfence();
         epi_bar();
-        if (threadIdx.x == 4 * 32) *fx_last = atomicAdd(&p.counters[t.m_blk * p.num_n_tiles + t.n_blk], 1) == p.num_splits - 1;
-        epi_bar();
-        if (*fx_last) {
-          __threadfence();
-          split_fixup(p, row, t.n_blk);
-        }
+        if (threadIdx.x == 4 * 32 &&
+            atomicAdd(&p.counters[t.m_blk * p.num_n_tiles + t.n_blk], 1) == p.num_splits - 1)
+          fx_list[(*fx_count)++] = (t.prob << 24) | (t.n_blk << 16) | t.m_blk;
       }
       if (g.trace && threadIdx.x == 4 * 32) g.trace[8 * u + 3] = globaltimer();
     }
     if constexpr (EPI == 3) {
       if (lane == 0) bulk_wait_all();  // stores complete before the CTA retires
       __syncwarp();
+    }
+    if constexpr (EPI != 3) {
+      epi_bar();
+      const int nfx = *fx_count;
+      if (nfx > 0) {
+        __threadfence();  // the other splits' slab rows (fenced before their arrival counts)
+        for (int f = 0; f < nfx; ++f) {
+          const int e = fx_list[f];
+          const Prob& p = g.p[e >> 24];
+          const int m_blk = e & 0xFFFF, n_blk = (e >> 16) & 0xFF;
+          split_fixup(p, m_blk * kBM + q * 32 + lane, n_blk);
+        }
+      }
     }
   }
   tc_fence_before();

@@ -9,7 +9,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2312_03415_b200 import runlora as rl  # noqa: E402
 
+# ragged bf16; K-split Z blocks + repeated concat tails + in-kernel split fix-up (n = 1024,
+# k = m = 512, r = 16: 4 blocks); fp32
 for c in (synth.case("san_bf16", 0, 30, 300, 264, 200, 16, "bf16"),
+          synth.case("san_zsplit", 0, 32, 1024, 512, 512, 16, "bf16"),
           synth.case("san_f32", 0, 31, 70, 40, 56, 5, "f32")):
     d = {k: v.cuda() for k, v in synth.operands(c).items()}
     h = rl.handle(0)
