@@ -56,6 +56,15 @@ Ctx::Ctx(int device) : device_(device) {
       identity_ = nullptr;
     }
   }
+  {
+    std::vector<uint8_t> eye8(128 * 128, 0);
+    for (int i = 0; i < 128; ++i) eye8[i * 128 + i] = 0x38;  // E4M3 1.0
+    if (cudaMalloc(&identity8_, eye8.size()) != cudaSuccess ||
+        cudaMemcpy(identity8_, eye8.data(), eye8.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+      if (identity8_) cudaFree(identity8_);
+      identity8_ = nullptr;
+    }
+  }
   if (prev >= 0) cudaSetDevice(prev);
 }
 
@@ -67,12 +76,14 @@ Ctx::~Ctx() {
   for (auto e : free_events_) cudaEventDestroy(e);
   if (cur_start_) cudaEventDestroy(cur_start_);
   if (identity_) cudaFree(identity_);
+  if (identity8_) cudaFree(identity8_);
   if (trace) cudaFree(trace);
   if (ltrace_) cudaFree(ltrace_);
 }
 
-bool Ctx::tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* err, int swz, int chunks) {
-  const TmapKey key{m.ptr, m.rows, m.cols, m.ld, box_rows, swz, chunks};
+bool Ctx::tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* err, int swz, int chunks,
+               int elem) {
+  const TmapKey key{m.ptr, m.rows, m.cols, m.ld, box_rows, swz, chunks, elem};
   {
     std::lock_guard<std::mutex> g(tmap_mu_);
     auto it = tmaps_.find(key);
@@ -85,22 +96,23 @@ bool Ctx::tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* 
     if (err) *err = "cuTensorMapEncodeTiled entry point unavailable";
     return false;
   }
-  const cuuint32_t w = swz == 0 ? 128u : (cuuint32_t)(swz / 2);  // swz 0: no swizzle, 256-byte rows
+  const cuuint32_t w = swz == 0 ? 256u / elem : (cuuint32_t)(swz / elem);  // swz 0: no swizzle, 256-byte rows
   cuuint64_t dims[3] = {(cuuint64_t)m.cols, (cuuint64_t)m.rows, 1};
-  cuuint64_t strides[2] = {(cuuint64_t)m.ld * 2, 0};
+  cuuint64_t strides[2] = {(cuuint64_t)m.ld * elem, 0};
   cuuint32_t box[3] = {w, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1u, 1u, 1u};
   cuuint32_t rank = 2;
   if (chunks > 0) {
     dims[0] = w;
     dims[2] = (cuuint64_t)(m.cols / w);
-    strides[1] = (cuuint64_t)w * 2;
+    strides[1] = (cuuint64_t)w * elem;
     box[2] = (cuuint32_t)chunks;
     rank = 3;
   }
   CUtensorMap tm;
   CUresult r = reinterpret_cast<EncodeTiledFn>(encode_fn_)(
-      &tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(m.ptr), dims, strides, box, estr,
+      &tm, elem == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
+      const_cast<void*>(m.ptr), dims, strides, box, estr,
       CU_TENSOR_MAP_INTERLEAVE_NONE,
       swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
       : swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B

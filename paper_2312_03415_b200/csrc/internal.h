@@ -26,7 +26,7 @@ enum KernelId : int {
   KID_SPLITK_REDUCE,   // fixed-order split-K reduction / cast / transpose
   KID_SGEMM_F32,       // fp32 SIMT GEMM (RUNLORA_F32 path)
   KID_QUANT,           // W -> FP8 E4M3 + per-column scales (column max, quantize, finalize)
-  KID_DEQUANT,         // FP8 E4M3 W -> bf16 W in the workspace (QLoRA-style entry points)
+  KID_DEQUANT,         // W~ = bf16(e4m3(Wq)·scale) via the FP8 identity-tail GEMM (x1 variants' W)
   KID_ALLREDUCE,       // one-shot fixed-order allreduce of [dA | dB] over peer pointers
   KID_COUNT
 };
@@ -75,6 +75,11 @@ struct GemmReq {
   bool fx_transpose, fx_accumulate, fx_bf16;
   int* zero_ptr;  // launch-level (first request): ints zeroed by CTA 0 after the PDL wait
   int zero_n;
+  // FP8 identity tail (Prob::tail_fp8): a2 = E4M3 identity, b2 = Wq (uint8), K2 = 128;
+  // out_mode OUT_BF16_WQ with one scale per output row (wq_row_scale) or column
+  bool tail_fp8;
+  const float* wq_scale;
+  bool wq_row_scale;
 };
 
 struct ReduceJob {
@@ -100,6 +105,8 @@ class Ctx {
   bool pdl() const { return pdl_; }    // programmatic dependent launch (env RUNLORA_PDL=0 disables)
   // 128x128 bf16 identity (device): A operand of the block-diagonal tail that adds W in W + A·B
   const void* identity() const { return identity_; }
+  // 128x128 E4M3 identity (1.0 = 0x38): A operand of the FP8 tail that dequantises Wq (R18)
+  const void* identity8() const { return identity8_; }
   // debug timeline buffer (env RUNLORA_TRACE=<kernel id>): see GemmArgs::trace
   unsigned long long* trace = nullptr;
   unsigned long long* ltrace_ = nullptr;
@@ -126,7 +133,7 @@ class Ctx {
   // chunks > 0: 3-D view {swz/2, rows, cols/(swz/2)} (chunk stride swz bytes), box
   // {swz/2, box_rows, chunks} -> one TMA op fills `chunks` adjacent swizzle columns.
   bool tmap(const DeviceMat& m, int box_rows, CUtensorMap* out, std::string* err, int swz_bytes = 128,
-            int chunks = 0);
+            int chunks = 0, int elem_bytes = 2);  // elem_bytes 1: an E4M3 (uint8) matrix
 
   // Launch timeline (env RUNLORA_LTRACE=1): each launch gets a device slot of 8 words
   // {min CTA entry, min ready, max ready, min exit, max exit} (%globaltimer ns; "ready" =
@@ -155,6 +162,7 @@ class Ctx {
   int num_sms_ = 148;
   int main_cg_ = 2;
   void* identity_ = nullptr;
+  void* identity8_ = nullptr;
   bool tma_store_main_ = false;   // env RUNLORA_TMA_STORE_MAIN=1
   bool main_wide_ = true;
   double wide_cost_a_ = 1.66, wide_cost_e_ = 443.0;
@@ -168,16 +176,16 @@ class Ctx {
   struct TmapKey {
     const void* ptr;
     int64_t rows, cols, ld;
-    int box_rows, swz, chunks;
+    int box_rows, swz, chunks, elem;
     bool operator==(const TmapKey& o) const {
       return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && box_rows == o.box_rows &&
-             swz == o.swz && chunks == o.chunks;
+             swz == o.swz && chunks == o.chunks && elem == o.elem;
     }
   };
   struct TmapKeyHash {
     size_t operator()(const TmapKey& k) const {
       size_t h = std::hash<const void*>()(k.ptr);
-      for (int64_t v : {k.rows, k.cols, k.ld, (int64_t)k.box_rows, (int64_t)k.swz, (int64_t)k.chunks})
+      for (int64_t v : {k.rows, k.cols, k.ld, (int64_t)k.box_rows, (int64_t)k.swz, (int64_t)k.chunks, (int64_t)k.elem})
         h = h * 1000003u ^ std::hash<int64_t>()(v);
       return h;
     }
@@ -213,8 +221,7 @@ cudaError_t launch_quantize_w(Ctx& ctx, const void* W, int64_t k, int64_t m, voi
 constexpr int kMaxPeers = 16;  // runlora_allreduce_sum_f32
 cudaError_t launch_allreduce_sum_f32(Ctx& ctx, const float* const* peers, int P, float* out, int64_t n,
                                      cudaStream_t s);
-cudaError_t launch_dequantize_w(Ctx& ctx, const void* Wq, const float* scale, int64_t k, int64_t m, void* W,
-                                cudaStream_t s);
+
 // fp32 SIMT GEMM: C[i,j] = (acc ? C[i,j] : 0) + (Cadd ? Cadd[i,j] : 0) + sum_t A(i,t) B(t,j),
 // A(i,t) = A[i*sa0 + t*sa1], B(t,j) = B[t*sb0 + j*sb1].
 cudaError_t launch_sgemm(Ctx& ctx, int M, int N, int K, const float* A, int64_t sa0, int64_t sa1, const float* B,

@@ -274,7 +274,8 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
       if (err) *err = "tc_gemm: 512-wide tiles need a CTA pair, K-major B and a plain output";
       return cudaErrorInvalidValue;
     }
-    if (r.tma_store && (r.out_mode != OUT_BF16 || r.BN < 256 || r.splits > 1)) {
+    if (r.tma_store && (!(r.out_mode == OUT_BF16 || (r.out_mode == OUT_BF16_WQ && r.tail_fp8)) ||
+                        (r.BN < 256 && !r.tail_fp8) || r.splits > 1)) {
       if (err) *err = "tc_gemm: TMA-store epilogue needs a plain bf16 output with 256- or 512-wide tiles";
       return cudaErrorInvalidValue;
     }
@@ -296,7 +297,13 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
     if (!ctx.tmap(r.a, a_box, &tm.m[q][0], err, 128, a3 ? 2 : 0) ||
         !ctx.tmap(r.b, b_box, &tm.m[q][1], err, b_swz, b3 ? nb / b_cw : 0))
       return cudaErrorInvalidValue;
-    if (r.K2 > 0) {
+    if (r.tail_fp8) {  // E4M3 identity and Wq: boxes of 128 rows x 128 bytes
+      if (r.K2 != 128 || cg != 1 || r.BN > 128 || r.out_mode != OUT_BF16_WQ || !r.tma_store || !r.wq_scale ||
+          !ctx.tmap(r.a2, 128, &tm.m[q][2], err, 128, 0, 1) || !ctx.tmap(r.b2, 128, &tm.m[q][3], err, 128, 0, 1)) {
+        if (err && err->empty()) *err = "tc_gemm: the FP8 tail needs K2 = 128, BN <= 128, one CTA, the WQ epilogue";
+        return cudaErrorInvalidValue;
+      }
+    } else if (r.K2 > 0) {
       if (!ctx.tmap(r.a2, a_box, &tm.m[q][2], err, 128, a3 ? 2 : 0) ||
           !ctx.tmap(r.b2, b_box, &tm.m[q][3], err, b_swz, b3 ? nb / b_cw : 0))
         return cudaErrorInvalidValue;
@@ -345,6 +352,13 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
       return cudaErrorInvalidValue;
     }
     p.tail_diag = r.tail_diag ? 1 : 0;
+    if (r.tail_fp8) {
+      p.tail_fp8 = 1;
+      p.nk2 = 1;
+      p.idesc2 = idesc_e4m3(kBM, r.BN, r.a_mn, r.b_mn);
+      p.wq_scale = r.wq_scale;
+      p.wq_row_scale = r.wq_row_scale ? 1 : 0;
+    }
     if (r.tail_rep > 0) {
       if (r.K2 != r.tail_w || r.tail_w <= 0 || r.tail_w > kBK || r.tail_diag) {
         if (err) *err = "tc_gemm: a repeated tail needs K2 == tail_w <= 64";

@@ -244,6 +244,16 @@ __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64
         : "memory");
   }
 }
+// D[tmem] (+)= A[smem] * B[smem], kind::f8f6f4 (E4M3 inputs per the instruction descriptor,
+// fp32 accumulate; K = 32 per instruction).  Single-CTA only (the quantized-W' build).
+__device__ __forceinline__ void umma_f8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // Arrive (once) on `bar` when all previously issued tcgen05.mma of this thread complete.
 // CG = 2: multicast to the barrier at the same offset in both CTAs of the pair.
 template <int CG>
@@ -308,6 +318,16 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
   return (1u << 4)                       // c_format = F32
          | (1u << 7)                     // a_format = BF16
          | (1u << 10)                    // b_format = BF16
+         | ((a_mn ? 1u : 0u) << 15)      // a_major
+         | ((b_mn ? 1u : 0u) << 16)      // b_major
+         | ((uint32_t)(N >> 3) << 17)    // N >> 3
+         | ((uint32_t)(M >> 4) << 24);   // M >> 4
+}
+
+// Instruction descriptor for kind::f8f6f4 with E4M3 A and B: D fp32, majors, N, M
+// (a_format = b_format = 0 = E4M3).
+__host__ __device__ constexpr uint32_t idesc_e4m3(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4)                       // c_format = F32
          | ((a_mn ? 1u : 0u) << 15)      // a_major
          | ((b_mn ? 1u : 0u) << 16)      // b_major
          | ((uint32_t)(N >> 3) << 17)    // N >> 3

@@ -4,7 +4,9 @@
 //   colmax      scale[j] <- bits of max_i |W[i, j]|           (atomicMax on non-negative floats)
 //   quantize    Wq[i, j] = e4m3_rn_satfinite(W[i, j] / s[j]),  s[j] = amax > 0 ? amax/448 : 1
 //   finalize    scale[j] <- s[j]
-//   dequantize  W~[i, j] = bf16_rn(fp32(e4m3(Wq[i, j])) · scale[j])   (16 elements per thread)
+// The way back, W~[i, j] = bf16_rn(fp32(e4m3(Wq[i, j])) · scale[j]), is not a kernel of its own:
+// the tcgen05 GEMM's FP8 identity tail does it inside the W' / W'ᵀ / W~ builds (runlora.cu
+// wprime_q, tc_gemm.cuh Prob::tail_fp8).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
@@ -56,60 +58,6 @@ __global__ void __launch_bounds__(256) finalize_scale_kernel(float* __restrict__
   if (j < m) scale[j] = col_scale(scale[j]);  // amax bits (as float) -> scale
 }
 
-// Each thread owns one group of `per` (16, or 8 when m % 16 != 0) columns — its scales stay
-// in registers — and walks the rows with a stride of (threads / column groups).
-__global__ void __launch_bounds__(256) dequantize_kernel(const uint8_t* __restrict__ Wq, const float* __restrict__ scale,
-                                                         int64_t k, int64_t m, __nv_bfloat16* __restrict__ W,
-                                                         unsigned long long* lt) {
-  if (threadIdx.x == 0) ltrace_mark(lt, 0);
-  pdl_wait();
-  pdl_launch_dependents();
-  if (threadIdx.x == 0) ltrace_mark(lt, 1);
-  const int per = (m & 15) ? 8 : 16;
-  const int64_t groups = m / per;
-  const int64_t tid = blockIdx.x * 256ll + threadIdx.x, nthr = (int64_t)gridDim.x * 256;
-  const int64_t rstride = nthr / groups;
-  if (rstride > 0 && tid < rstride * groups) {
-    const int64_t j0 = (tid % groups) * per;
-    float s[16];
-#pragma unroll
-    for (int e = 0; e < 16; e += 4) {
-      if (e < per) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(scale + j0 + e));
-        s[e] = v.x, s[e + 1] = v.y, s[e + 2] = v.z, s[e + 3] = v.w;
-      }
-    }
-    for (int64_t i = tid / groups; i < k; i += rstride) {
-      uint8_t q[16];
-      if (per == 16) *reinterpret_cast<uint4*>(q) = __ldg(reinterpret_cast<const uint4*>(Wq + i * m + j0));
-      else *reinterpret_cast<uint2*>(q) = __ldg(reinterpret_cast<const uint2*>(Wq + i * m + j0));
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (h * 8 >= per) break;
-        uint4 out;
-        __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(&out);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int c = 8 * h + 2 * e;
-          const float x0 = __half2float(__half(__nv_cvt_fp8_to_halfraw(q[c], __NV_E4M3))) * s[c];
-          const float x1 = __half2float(__half(__nv_cvt_fp8_to_halfraw(q[c + 1], __NV_E4M3))) * s[c + 1];
-          o[e] = __floats2bfloat162_rn(x0, x1);
-        }
-        *reinterpret_cast<uint4*>(W + i * m + j0 + 8 * h) = out;
-      }
-    }
-  } else if (rstride == 0) {  // more column groups than threads: grid-stride over everything
-    for (int64_t g = tid; g < k * groups; g += nthr) {
-      const int64_t i = g / groups, j0 = (g % groups) * per;
-      for (int e = 0; e < per; ++e) {
-        const float x = __half2float(__half(__nv_cvt_fp8_to_halfraw(Wq[i * m + j0 + e], __NV_E4M3))) * scale[j0 + e];
-        W[i * m + j0 + e] = __float2bfloat16_rn(x);
-      }
-    }
-  }
-  if (threadIdx.x == 0) ltrace_mark(lt, 2);
-}
-
 template <typename... KArgs, typename... Args>
 cudaError_t launch(Ctx& ctx, KernelId kid, void (*kern)(KArgs...), dim3 grid, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -148,13 +96,6 @@ cudaError_t launch_quantize_w(Ctx& ctx, const void* W, int64_t k, int64_t m, voi
              static_cast<uint8_t*>(Wq));
   if (e != cudaSuccess) return e;
   return launch(ctx, KID_QUANT, finalize_scale_kernel, dim3(cols), s, scale, m);
-}
-
-cudaError_t launch_dequantize_w(Ctx& ctx, const void* Wq, const float* scale, int64_t k, int64_t m, void* W,
-                                cudaStream_t s) {
-  return launch(ctx, KID_DEQUANT, dequantize_kernel, dim3(elem_blocks(ctx, k * (m / ((m & 15) ? 8 : 16)))), s,
-                static_cast<const uint8_t*>(Wq), scale, k, m, static_cast<__nv_bfloat16*>(W),
-                ctx.ltrace_slot(KID_DEQUANT));
 }
 
 }  // namespace runlora

@@ -529,6 +529,53 @@ runlora_status_t wprime_t_bf16(Ctx& c, const runlora_shape_t& s, const void* W, 
   return gemm(c, q, st);
 }
 
+// ------------------------------------------------------------ quantized W (R18)
+// Wq [k, m] E4M3 bytes with one fp32 scale per column: W~ = bf16(fp32(e4m3(Wq))·scale).
+struct QW {
+  const void* q;
+  const float* scale;
+};
+
+// W' = W~ + A·B (transposed = false: [k, m], the dX operand of backward4/5), W'ᵀ (transposed:
+// [m, k], forward2's B operand), or W~ alone (ab = false: the x1 variants' W) straight from
+// the 1-byte Wq: ONE GEMM whose fp8 identity tail I·Wq (kind::f8f6f4, exact) lands in a second
+// accumulator that the epilogue scales — D = bf16(A·B + bf16(I·Wq · scale)), the rounding of
+// R18 — so W is read as 1 byte per element and no bf16 copy of W~ is written first.
+runlora_status_t wprime_q(Ctx& c, const runlora_shape_t& s, const QW& w, const void* A, const void* B, void* D,
+                          bool transposed, bool ab, cudaStream_t st) {
+  GemmReq q = base_req((int)(transposed ? s.m : s.k), (int)(transposed ? s.k : s.m),
+                       ab ? KID_GEMM_WPRIME : KID_DEQUANT);
+  if (!ab) {  // W~ only: no main K (the main operands are never loaded)
+    q.a = mat(c.identity(), 128, 128);
+    q.b = mat(c.identity(), 128, 128);
+    q.b_mn = true;
+    q.K1 = 0;
+  } else if (transposed) {  // D[j, i] = Σ_r B[r, j]·A[i, r] + s[j]·Wq[i, j]
+    q.a = mat(B, s.r, s.m);
+    q.a_mn = true;
+    q.b = mat(A, s.k, s.r);
+    q.K1 = (int)s.r;
+  } else {  // D[i, j] = Σ_r A[i, r]·B[r, j] + s[j]·Wq[i, j]
+    q.a = mat(A, s.k, s.r);
+    q.b = mat(B, s.r, s.m);
+    q.b_mn = true;
+    q.K1 = (int)s.r;
+  }
+  q.a2 = mat(c.identity8(), 128, 128);
+  q.b2 = mat(w.q, s.k, s.m);  // bytes: K-major for W'ᵀ (K = j'), MN-major for W' / W~ (K = i')
+  q.K2 = 128;
+  q.tail_diag = true;
+  q.tail_fp8 = true;
+  q.wq_scale = w.scale;
+  q.wq_row_scale = transposed;
+  q.out_mode = OUT_BF16_WQ;
+  q.D = D;
+  q.ldd = transposed ? s.k : s.m;
+  q.BN = 128;  // two accumulators (A·B and I·Wq) of 128 columns per TMEM slot
+  q.tma_store = true;
+  return gemm(c, q, st);
+}
+
 // ------------------------------------------------------------ 512-wide main-GEMM tiles
 // A 256x512 pair tile (two N = 256 MMAs per k-step sharing the A tile) moves 25 % fewer TMA
 // bytes per FLOP than a 256x256 one, and the main GEMM's time tracks those bytes (DESIGN.md
@@ -668,7 +715,7 @@ GemmReq main_req(Ctx& c, int M, int N) {
 
 // ------------------------------------------------------------ bf16 variants
 runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* X, const void* W, const void* A,
-                              const void* B, void* Y, Bufs& b, cudaStream_t st) {
+                              const void* B, void* Y, Bufs& b, cudaStream_t st, const QW* qw = nullptr) {
   const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
   GemmReq q = main_req(c, (int)n, (int)m);
   q.a = mat(X, n, k);
@@ -713,7 +760,8 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
       q.K2 = (int)r;
     }
   } else {
-    RL_TRY(wprime_t_bf16(c, s, W, A, B, b.wp, st));  // W'ᵀ [m, k]
+    if (qw) RL_TRY(wprime_q(c, s, *qw, A, B, b.wp, true, true, st));  // W'ᵀ [m, k] from Wq
+    else RL_TRY(wprime_t_bf16(c, s, W, A, B, b.wp, st));                // W'ᵀ [m, k]
     q.b = mat(b.wp, m, k);
     q.b_mn = false;
   }
@@ -837,7 +885,7 @@ runlora_status_t params_bf16(Ctx& c, int v, const runlora_shape_t& s, const void
 }
 
 runlora_status_t input_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* W, const void* A, const void* B,
-                            const void* dY, void* dX, Bufs& b, cudaStream_t st) {
+                            const void* dY, void* dX, Bufs& b, cudaStream_t st, const QW* qw = nullptr) {
   const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
   GemmReq q = main_req(c, (int)n, (int)k);
   q.overlaps_comm = true;  // backward_input runs while backward_params' allreduce is in flight
@@ -862,7 +910,8 @@ runlora_status_t input_bf16(Ctx& c, int v, const runlora_shape_t& s, const void*
       q.tail_w = (int)r;
     }
   } else {  // dX = dY·W'ᵀ
-    RL_TRY(wprime_bf16(c, s, W, A, B, b.wp, st));
+    if (qw) RL_TRY(wprime_q(c, s, *qw, A, B, b.wp, false, true, st));  // W' [k, m] from Wq
+    else RL_TRY(wprime_bf16(c, s, W, A, B, b.wp, st));
     q.b = mat(b.wp, k, m);
   }
   return main_gemm(c, q, b, st);
@@ -1305,15 +1354,14 @@ runlora_status_t runlora_allreduce_sum_f32(runlora_handle_t h, const float* cons
 runlora_status_t runlora_workspace_size_wq(const runlora_shape_t* s, int fwd, int bwd, size_t* bytes) {
   RL_TRY(runlora_workspace_size(s, fwd, bwd, bytes));
   if (s->dtype != RUNLORA_BF16) return fail(RUNLORA_ERR_DTYPE, "quantized W needs bf16 operands");
-  *bytes += al((size_t)s->k * s->m * 2);  // the dequantized W, after the regular workspace
+  *bytes += al((size_t)s->k * s->m * 2);  // W~ for the x1 variants, after the regular workspace
   return RUNLORA_OK;
 }
 
 namespace {
-// Dequantizes Wq into the tail of the workspace; returns the bf16 W and the regular
-// workspace size that precedes it.
-runlora_status_t dequant_into_ws(runlora_handle_t h, const runlora_shape_t* s, const void* Wq, const float* scale,
-                                 void* ws, size_t ws_bytes, void* stream, const void** W, size_t* ws_main) {
+// Validates the quantized-W arguments; binds the regular workspace and the W~ region after it.
+runlora_status_t bind_wq(runlora_handle_t h, const runlora_shape_t* s, const void* Wq, const float* scale, void* ws,
+                         size_t ws_bytes, Bufs* b, void** wdq) {
   RL_TRY(check_handle(h));
   RL_TRY(check_shape(s));
   if (s->dtype != RUNLORA_BF16) return fail(RUNLORA_ERR_DTYPE, "quantized W needs bf16 operands");
@@ -1322,39 +1370,56 @@ runlora_status_t dequant_into_ws(runlora_handle_t h, const runlora_shape_t* s, c
   if (!ws) return fail(RUNLORA_ERR_INVALID_ARG, "workspace is NULL");
   const size_t main = layout_of(*s).total;
   if (ws_bytes < main + al((size_t)s->k * s->m * 2)) {
-    char b[160];
-    snprintf(b, sizeof b, "workspace too small for the quantized-W entry points: %zu bytes given, %zu needed",
+    char buf[160];
+    snprintf(buf, sizeof buf, "workspace too small for the quantized-W entry points: %zu bytes given, %zu needed",
              ws_bytes, main + al((size_t)s->k * s->m * 2));
-    return fail(RUNLORA_ERR_WORKSPACE, b);
+    return fail(RUNLORA_ERR_WORKSPACE, buf);
   }
-  void* wdq = static_cast<char*>(ws) + main;
-  CallLock lk(h->ctx->call_mu);
-  DeviceGuard dg(h->ctx->device());
-  cudaError_t e = launch_dequantize_w(*h->ctx, Wq, scale, s->k, s->m, wdq, static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return cuda_fail(e, "dequantize launch");
-  *W = wdq;
-  *ws_main = main;
+  RL_TRY(bind_ws(*s, ws, main, b));
+  *wdq = static_cast<char*>(ws) + main;
   return RUNLORA_OK;
 }
 }  // namespace
 
+// forward2 builds W'ᵀ straight from Wq (one fused launch); forward1 needs W~ itself as its
+// main B operand: the same converter writes it into the workspace tail first.
 runlora_status_t runlora_forward_wq(runlora_handle_t h, int fwd, const runlora_shape_t* s, const void* X,
                                     const void* Wq, const float* scale, const void* A, const void* B, void* Y,
                                     void* ws, size_t ws_bytes, void* stream) {
-  const void* W = nullptr;
-  size_t main = 0;
-  RL_TRY(dequant_into_ws(h, s, Wq, scale, ws, ws_bytes, stream, &W, &main));
-  return do_forward(h, fwd, s, X, W, A, B, Y, ws, main, stream);
+  Bufs b;
+  void* wdq = nullptr;
+  RL_TRY(bind_wq(h, s, Wq, scale, ws, ws_bytes, &b, &wdq));
+  RL_TRY(validate_forward(h, fwd, s, X, wdq, A, B, Y));
+  CallLock lk(h->ctx->call_mu);
+  DeviceGuard dg(h->ctx->device());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const QW qw{Wq, scale};
+  if (fwd == 1) RL_TRY(wprime_q(*h->ctx, *s, qw, nullptr, nullptr, wdq, false, false, st));
+  RL_TRY(forward_bf16(*h->ctx, fwd, *s, X, wdq, A, B, Y, b, st, fwd == 2 ? &qw : nullptr));
+  return post_launch();
 }
 
+// backward4/5 build W' straight from Wq for dX; backward1..3 multiply dX by W~ itself
+// (converter into the workspace tail); the adapter gradients never touch W.
 runlora_status_t runlora_backward_wq(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X,
                                      const void* Wq, const float* scale, const void* A, const void* B,
                                      const void* dY, void* dX, void* dA, void* dB, int grad_dtype, int accumulate,
                                      void* ws, size_t ws_bytes, void* stream) {
-  const void* W = nullptr;
-  size_t main = 0;
-  RL_TRY(dequant_into_ws(h, s, Wq, scale, ws, ws_bytes, stream, &W, &main));
-  return do_backward(h, bwd, s, X, W, A, B, dY, dX, dA, dB, grad_dtype, accumulate, ws, main, stream);
+  Bufs b;
+  void* wdq = nullptr;
+  RL_TRY(bind_wq(h, s, Wq, scale, ws, ws_bytes, &b, &wdq));
+  RL_TRY(validate_params(h, bwd, s, X, A, B, dY, dA, dB, grad_dtype));
+  if (dX) RL_TRY(validate_input(h, bwd, s, wdq, A, B, dY, dX));
+  CallLock lk(h->ctx->call_mu);
+  DeviceGuard dg(h->ctx->device());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const QW qw{Wq, scale};
+  RL_TRY(params_bf16(*h->ctx, bwd, *s, X, A, B, dY, dA, dB, grad_dtype == RUNLORA_BF16, accumulate != 0, b, st));
+  if (dX) {
+    if (bwd <= 3) RL_TRY(wprime_q(*h->ctx, *s, qw, nullptr, nullptr, wdq, false, false, st));
+    RL_TRY(input_bf16(*h->ctx, bwd, *s, wdq, A, B, dY, dX, b, st, bwd >= 4 ? &qw : nullptr));
+  }
+  return post_launch();
 }
 
 runlora_status_t runlora_step_host(runlora_handle_t h, const runlora_shape_t* s, const runlora_host_step_t* t,
