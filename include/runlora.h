@@ -216,9 +216,13 @@ runlora_status_t runlora_step_host(runlora_handle_t h, const runlora_shape_t* s,
  * runlora_quantize_w_e4m3: W bf16 [k, m] (device) -> Wq, scale (device; scale 16-byte
  *   aligned, m a multiple of 8).  Asynchronous on `stream`.
  * runlora_forward_wq / runlora_backward_wq: as runlora_forward / runlora_backward with W
- *   given as (Wq, scale); every call dequantizes W~ into the workspace (after the regular
- *   workspace) and runs the unchanged variants on it, so only Wq + scale persist between
- *   calls (half of the bf16 W).  Workspace: runlora_workspace_size_wq bytes. */
+ *   given as (Wq, scale); only Wq + scale persist between calls (half of the bf16 W).  The
+ *   dequantization rides in the tensor cores: forward2's W'ᵀ and backward4/5's W' are built
+ *   straight from the 1-byte Wq by one GEMM whose FP8 identity tail (I·Wq, exact) lands in a
+ *   second accumulator scaled in the epilogue, D = bf16(A·B + W~); forward1 and backward1..3,
+ *   which multiply by W~ itself, get it from the same GEMM without the A·B part, written
+ *   after the regular workspace.  m must be a multiple of 16 (16-byte row strides of Wq),
+ *   else RUNLORA_ERR_ALIGNMENT.  Workspace: runlora_workspace_size_wq bytes. */
 runlora_status_t runlora_quantize_w_e4m3(runlora_handle_t h, int64_t k, int64_t m, const void* W, void* Wq,
                                          float* scale, void* stream);
 runlora_status_t runlora_workspace_size_wq(const runlora_shape_t* s, int fwd, int bwd, size_t* bytes);

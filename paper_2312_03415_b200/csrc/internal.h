@@ -37,6 +37,18 @@ struct DeviceMat {  // row-major bf16 matrix view: element (i, j) at ptr[i*ld + 
   int64_t rows, cols, ld;
 };
 
+struct ReduceJob {
+  const float* P;
+  int splits;
+  int64_t split_stride;
+  int rows, cols;
+  int64_t ldp;
+  void* out;
+  int out_bf16;
+  int64_t ldo;
+  int transpose, accumulate;
+};
+
 struct GemmReq {
   int M, N;
   DeviceMat a;
@@ -75,6 +87,10 @@ struct GemmReq {
   bool fx_transpose, fx_accumulate, fx_bf16;
   int* zero_ptr;  // launch-level (first request): ints zeroed by CTA 0 after the PDL wait
   int zero_n;
+  // launch-level (first request): up to 2 fixed-order split-K reductions run by the launch's
+  // idle warps 2-3 (GemmArgs::side), e.g. the adapter-gradient slabs under the dX GEMM
+  const ReduceJob* side;
+  int nside;
   // FP8 identity tail (Prob::tail_fp8): a2 = E4M3 identity, b2 = Wq (uint8), K2 = 128;
   // out_mode OUT_BF16_WQ with one scale per output row (wq_row_scale) or column
   bool tail_fp8;
@@ -82,17 +98,6 @@ struct GemmReq {
   bool wq_row_scale;
 };
 
-struct ReduceJob {
-  const float* P;
-  int splits;
-  int64_t split_stride;
-  int rows, cols;
-  int64_t ldp;
-  void* out;
-  int out_bf16;
-  int64_t ldo;
-  int transpose, accumulate;
-};
 
 class Ctx {
  public:

@@ -56,7 +56,11 @@ cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, GemmArgs& g, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
   }
-  const int groups_max = ctx.num_sms() * OCC / CG;
+  int groups_max = ctx.num_sms() * OCC / CG;
+  // debug (env RUNLORA_MAX_CTAS): cap the persistent grid of the non-main kernels, e.g. to
+  // measure what a few SMs' worth of CTAs stream
+  static const int max_ctas = getenv("RUNLORA_MAX_CTAS") ? atoi(getenv("RUNLORA_MAX_CTAS")) : 0;
+  if (max_ctas > 0 && CG == 1 && BN < 256) groups_max = std::min(groups_max, max_ctas);
   const int groups = g.total_units < groups_max ? g.total_units : groups_max;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(groups * CG);
@@ -93,7 +97,9 @@ cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, GemmArgs& g, cudaStream_t s) {
 cudaError_t dispatch_tc(Ctx& ctx, int bn_max, int cg, bool occ2, bool tma_store, const Tmaps& tm, GemmArgs& g,
                         cudaStream_t s) {
   if (tma_store) {
-    if (cg == 1 && bn_max == 256) return run_tc<256, 1, 1, 3>(ctx, tm, g, s);
+    // (the quantized-W builds run 128-wide units on this 256-wide kernel: two accumulators of
+    // 128 columns per TMEM slot, Prob::tail_fp8)
+    if (cg == 1 && bn_max <= 256) return run_tc<256, 1, 1, 3>(ctx, tm, g, s);
     if (cg == 2 && bn_max == 256) return run_tc<256, 2, 1, 3>(ctx, tm, g, s);
     if (cg == 2 && bn_max == 512) return run_tc<512, 2, 1, 3>(ctx, tm, g, s);
     return cudaErrorNotSupported;
@@ -390,6 +396,14 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
     if (r.BN > bn_max) bn_max = r.BN;
   }
   g.nprob = nreq;
+  if (reqs[0].nside < 0 || reqs[0].nside > 2) return cudaErrorInvalidValue;
+  for (int j = 0; j < reqs[0].nside; ++j) {
+    const ReduceJob& J = reqs[0].side[j];
+    if (J.ldp % 4 || J.split_stride % 4) return cudaErrorInvalidValue;  // float4 slab reads
+    g.side[j] = SideJob{J.P, J.split_stride, J.ldp, J.ldo, J.out, J.splits, J.rows, J.cols, J.out_bf16, J.transpose,
+                        J.accumulate};
+  }
+  g.nside = reqs[0].nside;
   g.zero_ptr = reqs[0].zero_ptr;
   g.zero_n = reqs[0].zero_ptr ? reqs[0].zero_n : 0;
   g.trace = (ctx.trace && ctx.trace_kid == reqs[0].kid && g.total_units <= Ctx::kTraceUnits) ? ctx.trace : nullptr;

@@ -218,9 +218,11 @@ GemmReq base_req(int M, int N, KernelId kid) {
 // each output tile to finish sums the slabs in split order (Prob::fixup, deterministic).
 // The fix-up counters (per output tile) are zeroed by a memset node ahead of the launch —
 // this path serves shapes off the hot configurations (small n, backward2..4); the backward1/5
-// hot path zeroes them inside its projection launch instead (grads_tok_bf16).
+// hot path zeroes them inside its projection launch instead (grads_tok_bf16).  With `defer`
+// the slabs are not reduced here: their ReduceJobs are returned for the idle warps of the dX
+// GEMM launch that follows (do_backward).
 runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, int* counters, KernelId kid,
-                            cudaStream_t st) {
+                            cudaStream_t st, std::vector<ReduceJob>* defer = nullptr) {
   const SkinnyPlan p = plan_skinny(jobs, n);
   GemmReq q[2];
   int ntiles = 0;
@@ -246,6 +248,11 @@ runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, int* co
       q[i].split_stride = j.rows * (int64_t)p.Npad[i];
       q[i].splits = p.splits[i];
       q[i].kb_per_split = p.kps[i];
+      if (defer) {  // reduced by the idle warps of a later launch (see do_backward)
+        defer->push_back(ReduceJob{Pi, p.splits[i], j.rows * (int64_t)p.Npad[i], (int)j.rows, (int)j.r, p.Npad[i],
+                                   j.out, j.out_bf16 ? 1 : 0, j.ldo, j.transpose ? 1 : 0, j.accumulate ? 1 : 0});
+        continue;
+      }
       q[i].fixup = true;
       q[i].counters = counters + ntiles;
       q[i].fx_out = j.out;
@@ -257,7 +264,7 @@ runlora_status_t run_skinny(Ctx& c, const Skinny* jobs, int n, float* P, int* co
       ntiles += (int)(((j.rows + kBM - 1) / kBM) * (p.Npad[i] / p.BN[i]));
     }
   }
-  if (!p.direct) {
+  if (!p.direct && ntiles > 0) {
     cudaError_t e = cudaMemsetAsync(counters, 0, sizeof(int) * (size_t)ntiles, st);
     if (e != cudaSuccess) return cuda_fail(e, "fix-up counter reset");
   }
@@ -768,11 +775,13 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
   return main_gemm(c, q, b, st);
 }
 
-// backward1/5 adapter gradients: projections launch, then reductions launch whose last split
-// per output tile sums the token-split slabs in fixed order (see ZPlan; no reducer launch).
+// backward1/5 adapter gradients: projections launch, then reductions launch whose token-split
+// slabs are summed in fixed order either by the reductions launch itself (the last split per
+// output tile, Prob::fixup) or, with `defer`, by the idle warps of the dX GEMM launch that
+// follows (no reducer launch either way; see ZPlan).
 runlora_status_t grads_tok_bf16(Ctx& c, const ZPlan& f, const runlora_shape_t& s, const void* X, const void* A,
                                 const void* B, const void* dY, void* dA, void* dB, bool gb, bool acc, Bufs& b,
-                                cudaStream_t st) {
+                                cudaStream_t st, std::vector<ReduceJob>* defer) {
   const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
   const int zc = (int)(r * f.sz);  // columns of the partial-Z matrices
   const int tiles[2] = {(int)((k + kBM - 1) / kBM), (int)((m + kBM - 1) / kBM)};  // reduction output tiles
@@ -799,8 +808,10 @@ runlora_status_t grads_tok_bf16(Ctx& c, const ZPlan& f, const runlora_shape_t& s
     g.splits = f.sz;
     g.kb_per_split = f.kpz[i];
   }
-  q[0].zero_ptr = b.cnt;
-  q[0].zero_n = tiles[0] + tiles[1];
+  if (!defer) {
+    q[0].zero_ptr = b.cnt;
+    q[0].zero_n = tiles[0] + tiles[1];
+  }
   cudaError_t e = launch_tc_gemm(c, q, 2, st, &err);
   if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
   // reductions: dA = Σ_s Xᵀ·Z1_s, dBᵀ = Σ_s dYᵀ·Z2_s (token splits -> fp32 slabs, fixed-order
@@ -832,6 +843,11 @@ runlora_status_t grads_tok_bf16(Ctx& c, const ZPlan& f, const runlora_shape_t& s
       g.ldd = f.bn_t;  // plain slabs keep the padded tile width
     }
     g.split_stride = rows[i] * g.ldd;
+    if (defer) {  // the idle warps of the dX GEMM launch reduce the slabs (do_backward)
+      defer->push_back(ReduceJob{P, f.tsplits, g.split_stride, (int)rows[i], (int)r, g.ldd, outs[i], gb ? 1 : 0,
+                                 i == 0 ? r : m, i == 1 ? 1 : 0, acc ? 1 : 0});
+      continue;
+    }
     g.fixup = true;
     g.counters = b.cnt + (i == 0 ? 0 : tiles[0]);
     g.fx_out = outs[i];
@@ -847,15 +863,16 @@ runlora_status_t grads_tok_bf16(Ctx& c, const ZPlan& f, const runlora_shape_t& s
 }
 
 runlora_status_t params_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* X, const void* A, const void* B,
-                             const void* dY, void* dA, void* dB, bool gb, bool acc, Bufs& b, cudaStream_t st) {
+                             const void* dY, void* dA, void* dB, bool gb, bool acc, Bufs& b, cudaStream_t st,
+                             std::vector<ReduceJob>* defer = nullptr) {
   const int64_t n = s.n, k = s.k, m = s.m;
   if (v == 1 || v == 5) {  // Alg. 1 / Alg. 5: Z1, Z2 | dA = Xᵀ·Z1, dB = Z2ᵀ·dY
     const ZPlan f = plan_z(s);
-    if (f.ok) return grads_tok_bf16(c, f, s, X, A, B, dY, dA, dB, gb, acc, b, st);
+    if (f.ok) return grads_tok_bf16(c, f, s, X, A, B, dY, dA, dB, gb, acc, b, st, defer);
     Skinny pj[2] = {job_Z1(s, dY, B, b.z1), job_Z2(s, X, A, b.z2)};
     RL_TRY(run_skinny(c, pj, 2, b.P, b.cnt, KID_GEMM_PROJ, st));
     Skinny tj[2] = {job_dA_tok(s, X, b.z1, dA, gb, acc), job_dB_tok(s, dY, b.z2, dB, gb, acc)};
-    return run_skinny(c, tj, 2, b.P, b.cnt, KID_GEMM_TOKRED, st);
+    return run_skinny(c, tj, 2, b.P, b.cnt, KID_GEMM_TOKRED, st, defer);
   }
   if (v == 2 || v == 3) {  // Z1 = dY·Bᵀ
     Skinny j = job_Z1(s, dY, B, b.z1);
@@ -877,17 +894,22 @@ runlora_status_t params_bf16(Ctx& c, int v, const runlora_shape_t& s, const void
   }
   if (v == 2) {  // dA = Xᵀ·Z1, dB = Aᵀ·Z2'
     Skinny j[2] = {job_dA_tok(s, X, b.z1, dA, gb, acc), job_dB_dense(s, b.wp, A, dB, gb, acc)};
-    return run_skinny(c, j, 2, b.P, b.cnt, KID_GEMM_SMALL, st);
+    return run_skinny(c, j, 2, b.P, b.cnt, KID_GEMM_SMALL, st, defer);
   }
   // v = 3, 4: dA = Z2'·Bᵀ, dB = Aᵀ·Z2'
   Skinny j[2] = {job_dA_dense(s, b.wp, B, dA, gb, acc), job_dB_dense(s, b.wp, A, dB, gb, acc)};
-  return run_skinny(c, j, 2, b.P, b.cnt, KID_GEMM_SMALL, st);
+  return run_skinny(c, j, 2, b.P, b.cnt, KID_GEMM_SMALL, st, defer);
 }
 
 runlora_status_t input_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* W, const void* A, const void* B,
-                            const void* dY, void* dX, Bufs& b, cudaStream_t st, const QW* qw = nullptr) {
+                            const void* dY, void* dX, Bufs& b, cudaStream_t st, const QW* qw = nullptr,
+                            const std::vector<ReduceJob>* side = nullptr) {
   const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
   GemmReq q = main_req(c, (int)n, (int)k);
+  if (side && !side->empty()) {  // the adapter gradients' slabs, reduced by this launch's idle warps
+    q.side = side->data();
+    q.nside = (int)side->size();
+  }
   q.overlaps_comm = true;  // backward_input runs while backward_params' allreduce is in flight
   q.a = mat(dY, n, m);
   q.a_mn = false;
@@ -1047,7 +1069,8 @@ runlora_status_t validate_input(runlora_handle_t h, int bwd, const runlora_shape
 
 runlora_status_t do_params(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X, const void* W,
                            const void* A, const void* B, const void* dY, void* dA, void* dB, int grad_dtype,
-                           int accumulate, void* ws, size_t ws_bytes, void* stream) {
+                           int accumulate, void* ws, size_t ws_bytes, void* stream,
+                           std::vector<ReduceJob>* defer = nullptr) {
   (void)W;
   RL_TRY(validate_params(h, bwd, s, X, A, B, dY, dA, dB, grad_dtype));
   Bufs b;
@@ -1056,21 +1079,23 @@ runlora_status_t do_params(runlora_handle_t h, int bwd, const runlora_shape_t* s
   DeviceGuard dg(h->ctx->device());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (s->dtype == RUNLORA_BF16)
-    RL_TRY(params_bf16(*h->ctx, bwd, *s, X, A, B, dY, dA, dB, grad_dtype == RUNLORA_BF16, accumulate != 0, b, st));
+    RL_TRY(params_bf16(*h->ctx, bwd, *s, X, A, B, dY, dA, dB, grad_dtype == RUNLORA_BF16, accumulate != 0, b, st,
+                       defer));
   else
     RL_TRY(params_f32(*h->ctx, bwd, *s, X, A, B, dY, dA, dB, accumulate != 0, b, st));
   return post_launch();
 }
 
 runlora_status_t do_input(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* W, const void* A,
-                          const void* B, const void* dY, void* dX, void* ws, size_t ws_bytes, void* stream) {
+                          const void* B, const void* dY, void* dX, void* ws, size_t ws_bytes, void* stream,
+                          const std::vector<ReduceJob>* side = nullptr) {
   RL_TRY(validate_input(h, bwd, s, W, A, B, dY, dX));
   Bufs b;
   RL_TRY(bind_ws(*s, ws, ws_bytes, &b));
   CallLock lk(h->ctx->call_mu);
   DeviceGuard dg(h->ctx->device());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (s->dtype == RUNLORA_BF16) RL_TRY(input_bf16(*h->ctx, bwd, *s, W, A, B, dY, dX, b, st));
+  if (s->dtype == RUNLORA_BF16) RL_TRY(input_bf16(*h->ctx, bwd, *s, W, A, B, dY, dX, b, st, nullptr, side));
   else RL_TRY(input_f32(*h->ctx, bwd, *s, W, A, B, dY, dX, b, st));
   return post_launch();
 }
@@ -1086,9 +1111,13 @@ runlora_status_t do_backward(runlora_handle_t h, int bwd, const runlora_shape_t*
     RL_TRY(bind_ws(*s, ws, ws_bytes, &b));
   }
   CallLock lk(h->ctx->call_mu);
-  // adapter gradients (reduced inside their own launches), then dX — one PDL chain
-  RL_TRY(do_params(h, bwd, s, X, W, A, B, dY, dA, dB, grad_dtype, accumulate, ws, ws_bytes, stream));
-  if (dX) RL_TRY(do_input(h, bwd, s, W, A, B, dY, dX, ws, ws_bytes, stream));
+  // adapter gradients, then dX — one PDL chain.  With dX, the adapter gradients' split-K slabs
+  // are reduced (fixed order) by the idle warps 2-3 of the dX GEMM launch, concurrently with
+  // its mainloop; without dX (or in the split _params call) their own launch reduces them.
+  std::vector<ReduceJob> side;
+  RL_TRY(do_params(h, bwd, s, X, W, A, B, dY, dA, dB, grad_dtype, accumulate, ws, ws_bytes, stream,
+                   dX && s->dtype == RUNLORA_BF16 ? &side : nullptr));
+  if (dX) RL_TRY(do_input(h, bwd, s, W, A, B, dY, dX, ws, ws_bytes, stream, &side));
   return RUNLORA_OK;
 }
 
@@ -1365,6 +1394,8 @@ runlora_status_t bind_wq(runlora_handle_t h, const runlora_shape_t* s, const voi
   RL_TRY(check_handle(h));
   RL_TRY(check_shape(s));
   if (s->dtype != RUNLORA_BF16) return fail(RUNLORA_ERR_DTYPE, "quantized W needs bf16 operands");
+  if (s->m & 15)
+    return fail(RUNLORA_ERR_ALIGNMENT, "quantized W needs m a multiple of 16 (16-byte TMA row strides of the 1-byte Wq)");
   RL_TRY(check_ptr(Wq, "Wq"));
   RL_TRY(check_ptr(scale, "scale"));
   if (!ws) return fail(RUNLORA_ERR_INVALID_ARG, "workspace is NULL");
@@ -1414,10 +1445,12 @@ runlora_status_t runlora_backward_wq(runlora_handle_t h, int bwd, const runlora_
   DeviceGuard dg(h->ctx->device());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const QW qw{Wq, scale};
-  RL_TRY(params_bf16(*h->ctx, bwd, *s, X, A, B, dY, dA, dB, grad_dtype == RUNLORA_BF16, accumulate != 0, b, st));
+  std::vector<ReduceJob> side;
+  RL_TRY(params_bf16(*h->ctx, bwd, *s, X, A, B, dY, dA, dB, grad_dtype == RUNLORA_BF16, accumulate != 0, b, st,
+                     dX ? &side : nullptr));
   if (dX) {
     if (bwd <= 3) RL_TRY(wprime_q(*h->ctx, *s, qw, nullptr, nullptr, wdq, false, false, st));
-    RL_TRY(input_bf16(*h->ctx, bwd, *s, wdq, A, B, dY, dX, b, st, bwd >= 4 ? &qw : nullptr));
+    RL_TRY(input_bf16(*h->ctx, bwd, *s, wdq, A, B, dY, dX, b, st, bwd >= 4 ? &qw : nullptr, &side));
   }
   return post_launch();
 }

@@ -107,8 +107,20 @@ struct Prob {
 constexpr int kMaxProb = 2;  // problems per launch (dual launches); kernel params stay ~1.8 KB
 constexpr int kTraceMaxUnits = 1 << 16;  // debug trace: unit records, then 4 words per CTA
 
+// A fixed-order split-K reduction carried by a GEMM launch as a side job of its otherwise idle
+// warps 2-3 (e.g. the adapter gradients' token-split slabs, reduced while the dX GEMM runs):
+//   out[i, c] (or out[c, i] when transpose) {=, +=} sum_{s < splits} P[s][i][c],  c < cols.
+struct SideJob {
+  const float* P;
+  long long split_stride, ldp, ldo;
+  void* out;
+  int splits, rows, cols, out_bf16, transpose, accumulate;
+};
+
 struct GemmArgs {
   Prob p[kMaxProb];
+  SideJob side[2];
+  int nside;
   int nprob;
   int total_units;
   int dbg;  // 0 normal; 1: no TMA (MMA-only); 2: no MMA (TMA-only); 3: as 1 + no stores; 4: as 1 + no epilogue;
@@ -306,6 +318,47 @@ __device__ __forceinline__ void split_fixup(const Prob& p, int row, int n_blk) {
 }
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// SideJob reduction by `nthr` threads (index tid) across the grid: one (row, 4-column group)
+// per item, the splits' float4 loads issued 8 at a time, summed in split order.
+__device__ __forceinline__ void side_reduce(const GemmArgs& g, long long tid, long long nthr) {
+  for (int j = 0; j < g.nside; ++j) {
+    const SideJob& J = g.side[j];
+    const int groups = (J.cols + 3) >> 2;
+    const long long total = (long long)J.rows * groups;
+    for (long long idx = tid; idx < total; idx += nthr) {
+      const int i = (int)(idx / groups), c0 = (int)(idx % groups) * 4;
+      const float4* src = reinterpret_cast<const float4*>(J.P + (long long)i * J.ldp + c0);
+      const long long st4 = J.split_stride >> 2;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s0 = 0; s0 < J.splits; s0 += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+          if (s0 + x < J.splits) v[x] = __ldcg(src + (s0 + x) * st4);
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+          if (s0 + x < J.splits) acc.x += v[x].x, acc.y += v[x].y, acc.z += v[x].z, acc.w += v[x].w;
+      }
+      const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        if (c0 + x >= J.cols) break;
+        const long long o = J.transpose ? (long long)(c0 + x) * J.ldo + i : (long long)i * J.ldo + c0 + x;
+        float val = a4[x];
+        if (J.out_bf16) {
+          __nv_bfloat16* d = static_cast<__nv_bfloat16*>(J.out) + o;
+          if (J.accumulate) val += __bfloat162float(*d);
+          *d = __float2bfloat16_rn(val);
+        } else {
+          float* d = static_cast<float*>(J.out) + o;
+          if (J.accumulate) val += *d;
+          *d = val;
+        }
+      }
+    }
+  }
+}
 
 // EPI = 3: one 32-row x 64-column bf16 chunk of a warp (row = lane) -> its staging buffer
 // (128B swizzle: 16-byte chunk e of row r at (e ^ (r & 7)) * 16) -> TMA store.  A buffer is
@@ -655,6 +708,9 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       }
       sc += nh;
     }
+  } else if ((warp == 2 || warp == 3) && g.nside > 0) {
+    // ----------------------------------------------- side job of the idle warps
+    side_reduce(g, (long long)blockIdx.x * 64 + (threadIdx.x - 64), (long long)gridDim.x * 64);
   } else if (warp >= 4) {
     // --------------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access

@@ -15,7 +15,8 @@ import threading
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "librunlora.so")
+# the in-tree build; RUNLORA_LIB overrides it (e.g. tools/ab_lib.py loads two builds side by side)
+LIB_PATH = os.environ.get("RUNLORA_LIB") or os.path.join(_PKG, "lib", "librunlora.so")
 
 F32, BF16 = 0, 1
 BY_FLOPS, BY_TIME, HYBRID = 0, 1, 2

@@ -32,7 +32,7 @@ def _np(t):
 
 
 CASES = [synth.case("q_tiles", 0, 30, 520, 512, 768, 16, "bf16"),
-         synth.case("q_ragged_r8", 0, 31, 1000, 1024, 264, 8, "bf16")]
+         synth.case("q_ragged_r8", 0, 31, 1000, 1024, 272, 8, "bf16")]
 
 
 @pytest.mark.parametrize("c", CASES, ids=lambda c: c.name)
@@ -126,3 +126,11 @@ def test_wq_errors(rl):
     with pytest.raises(rl.RunLoRAError) as e:
         h.forward_wq(1, shape, X, qw, A, B, Y, ws=small)
     assert e.value.status == 7
+    # the 1-byte Wq needs 16-byte row strides: m a multiple of 16 (bf16 W only needs 8)
+    s8 = rl.make_shape(64, 256, 264, 8, rl.BF16)
+    q8 = h.quantize_w(torch.randn(256, 264, device="cuda").to(torch.bfloat16))
+    with pytest.raises(rl.RunLoRAError) as e:
+        h.forward_wq(2, s8, X[:64, :256].contiguous(), q8, A[:256, :8].contiguous(), B[:8, :264].contiguous(),
+                     torch.empty(64, 264, device="cuda", dtype=torch.bfloat16),
+                     ws=torch.empty(rl.workspace_size_wq(s8), dtype=torch.uint8, device="cuda"))
+    assert e.value.status == 6
