@@ -47,7 +47,19 @@ struct ReduceJob {
   int out_bf16;
   int64_t ldo;
   int transpose, accumulate;
+  // > 0: not a reduction but a column repeat (side jobs only): out[i, t*cols + j] = src[i, j]
+  // for t < repeat, bf16 rows of `cols` (multiple of 8) elements, src = P (as bf16)
+  int repeat;
 };
+inline ReduceJob repeat_job(const void* src, int rows, int cols, int reps, void* dst) {
+  ReduceJob j{};
+  j.P = static_cast<const float*>(src);
+  j.rows = rows;
+  j.cols = cols;
+  j.out = dst;
+  j.repeat = reps;
+  return j;
+}
 
 struct GemmReq {
   int M, N;
@@ -76,7 +88,6 @@ struct GemmReq {
   bool tma_store;  // OUT_BF16 through the TMA-store epilogue (all problems of a launch alike)
   bool overlaps_comm;  // the dX GEMM, which a data-parallel allreduce overlaps: runs on
                        // RUNLORA_MAIN_STAGES (fewer ring stages leave shared memory for NCCL)
-  int tail_rep, tail_w;  // repeated concat-K tail (Prob::tail_rep): K2 = tail_w, tail_rep blocks
   // in-kernel split-K fix-up (Prob::fixup): the last split of each output tile reduces the
   // slabs into fx_out (the ReduceJob semantics); counters zeroed by an earlier launch
   bool fixup;

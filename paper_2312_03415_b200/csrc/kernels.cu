@@ -322,6 +322,7 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
       if (!ctx.tmap(dm, 32, &tm.m[q][4], err, 128)) return cudaErrorInvalidValue;
     }
     Prob& p = g.p[q];
+    ProbX& px = g.px[q];
     p.M = r.M;
     p.N = r.N;
     p.bn = r.BN;
@@ -359,35 +360,26 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
     }
     p.tail_diag = r.tail_diag ? 1 : 0;
     if (r.tail_fp8) {
-      p.tail_fp8 = 1;
+      px.tail_fp8 = 1;
       p.nk2 = 1;
-      p.idesc2 = idesc_e4m3(kBM, r.BN, r.a_mn, r.b_mn);
-      p.wq_scale = r.wq_scale;
-      p.wq_row_scale = r.wq_row_scale ? 1 : 0;
-    }
-    if (r.tail_rep > 0) {
-      if (r.K2 != r.tail_w || r.tail_w <= 0 || r.tail_w > kBK || r.tail_diag) {
-        if (err) *err = "tc_gemm: a repeated tail needs K2 == tail_w <= 64";
-        return cudaErrorInvalidValue;
-      }
-      p.tail_rep = r.tail_rep;
-      p.tail_w = r.tail_w;
-      p.nk2 = r.tail_rep;
+      px.idesc2 = idesc_e4m3(kBM, r.BN, r.a_mn, r.b_mn);
+      px.wq_scale = r.wq_scale;
+      px.wq_row_scale = r.wq_row_scale ? 1 : 0;
     }
     if (r.fixup) {
       if (!(r.out_mode == OUT_F32 || r.out_mode == OUT_F32_FOLD) || cg != 1 || !r.counters || !r.fx_out ||
-          r.ldd % 4 != 0) {
+          r.ldd % 4 != 0 || r.tma_store) {
         if (err) *err = "tc_gemm: the split fix-up needs an fp32 slab output, single-CTA tiles and counters";
         return cudaErrorInvalidValue;
       }
-      p.fixup = 1;
-      p.counters = r.counters;
-      p.fx_out = r.fx_out;
-      p.fx_ldo = r.fx_ldo;
-      p.fx_cols = r.fx_cols;
-      p.fx_transpose = r.fx_transpose;
-      p.fx_accumulate = r.fx_accumulate;
-      p.fx_bf16 = r.fx_bf16;
+      px.fixup = 1;
+      px.counters = r.counters;
+      px.fx_out = r.fx_out;
+      px.fx_ldo = r.fx_ldo;
+      px.fx_cols = r.fx_cols;
+      px.fx_transpose = r.fx_transpose;
+      px.fx_accumulate = r.fx_accumulate;
+      px.fx_bf16 = r.fx_bf16;
     }
     p.hint_a = r.a_policy == 1 ? kEvictNormal : r.a_policy == 2 ? kEvictFirst
                : r.a_stream_once ? kEvictFirst : kEvictNormal;
@@ -399,9 +391,10 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
   if (reqs[0].nside < 0 || reqs[0].nside > 2) return cudaErrorInvalidValue;
   for (int j = 0; j < reqs[0].nside; ++j) {
     const ReduceJob& J = reqs[0].side[j];
-    if (J.ldp % 4 || J.split_stride % 4) return cudaErrorInvalidValue;  // float4 slab reads
+    if (J.repeat > 0 ? (J.cols % 8 != 0) : (J.ldp % 4 || J.split_stride % 4))
+      return cudaErrorInvalidValue;  // 16-byte groups / float4 slab reads
     g.side[j] = SideJob{J.P, J.split_stride, J.ldp, J.ldo, J.out, J.splits, J.rows, J.cols, J.out_bf16, J.transpose,
-                        J.accumulate};
+                        J.accumulate, J.repeat};
   }
   g.nside = reqs[0].nside;
   g.zero_ptr = reqs[0].zero_ptr;
@@ -414,7 +407,7 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
   // drop from 4 to 3 (frees 48 KB) instead of being clamped to the full ring
   if (g.stages > 0 && g.stages < 7 && bn_max > 256) g.stages = 3;
   if (const char* d = getenv("RUNLORA_DBG_GEMM")) g.dbg = atoi(d);
-  for (int q = nreq; q < kMaxProb; ++q) g.p[q] = g.p[0], g.p[q].units = 0;
+  for (int q = nreq; q < kMaxProb; ++q) g.p[q] = g.p[0], g.px[q] = g.px[0], g.p[q].units = 0;
   if (g.total_units <= 0) return cudaSuccess;
   // a CTA defers at most kMaxFixups split fix-ups to the end of its unit loop; beyond that
   // (never on the shapes of the configs) the slabs are reduced by the reducer kernel instead
@@ -423,11 +416,12 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
   const int min_groups = ctx.num_sms() / cg;
   if ((g.total_units + min_groups - 1) / min_groups > kMaxFixups) {
     for (int q = 0; q < nreq; ++q) {
-      Prob& p = g.p[q];
-      if (!p.fixup) continue;
-      p.fixup = 0;
-      fallback[nfb++] = ReduceJob{static_cast<const float*>(p.D), p.num_splits, p.split_stride, p.M, p.fx_cols, p.ldd,
-                                  p.fx_out, p.fx_bf16, p.fx_ldo, p.fx_transpose, p.fx_accumulate};
+      const Prob& p = g.p[q];
+      ProbX& px = g.px[q];
+      if (!px.fixup) continue;
+      px.fixup = 0;
+      fallback[nfb++] = ReduceJob{static_cast<const float*>(p.D), p.num_splits, p.split_stride, p.M, px.fx_cols, p.ldd,
+                                  px.fx_out, px.fx_bf16, px.fx_ldo, px.fx_transpose, px.fx_accumulate};
     }
   }
   ctx.launch_begin(s, reqs[0].kid);

@@ -427,7 +427,7 @@ size_t main_split_bytes(const runlora_shape_t& s) {
 }
 
 struct Layout {
-  size_t z1, z2, cnt, wp, p, pm, total;
+  size_t z1, z2, arep, brep, cnt, wp, p, pm, total;
 };
 
 // Split fix-up counters: one int per output tile of a split rank-r launch (both problems).
@@ -436,7 +436,10 @@ size_t counter_count(const runlora_shape_t& s) {
   return (size_t)(2 * ((rows + kBM - 1) / kBM) * ((s.r + 15) / 16) + 64);
 }
 
-// Z1, Z2: n x r (or n x sz*r partial blocks, see ZPlan); cnt: split fix-up counters.
+// Z1, Z2: n x r (or n x sz*r partial blocks, see ZPlan); arep: A repeated sz times along its
+// columns (k x sz*r, backward1's dX tail against Z1's blocks); brep: B stacked szf times
+// (szf*r x m, forward1's Y tail against Z2's blocks) — both written by the idle warps of the
+// projection launch before them; cnt: split fix-up counters.
 Layout layout_of(const runlora_shape_t& s) {
   const size_t es = s.dtype == RUNLORA_BF16 ? 2 : 4;
   const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
@@ -446,7 +449,9 @@ Layout layout_of(const runlora_shape_t& s) {
   Layout L;
   L.z1 = 0;
   L.z2 = al((size_t)n * zc * es);
-  L.cnt = L.z2 + al((size_t)n * zc2 * es);
+  L.arep = L.z2 + al((size_t)n * zc2 * es);
+  L.brep = L.arep + (f.ok && f.sz > 1 ? al((size_t)k * zc * es) : 0);
+  L.cnt = L.brep + (f.ok && f.szf > 1 ? al((size_t)m * r * f.szf * es) : 0);
   L.wp = L.cnt + al(4 * counter_count(s));
   L.p = L.wp + al((size_t)k * m * es);
   L.pm = L.p + (s.dtype == RUNLORA_BF16 ? partial_need(s) : 0);  // main-GEMM split-K slabs after
@@ -455,7 +460,7 @@ Layout layout_of(const runlora_shape_t& s) {
 }
 
 struct Bufs {
-  void *z1, *z2, *wp;
+  void *z1, *z2, *arep, *brep, *wp;
   int* cnt;   // split fix-up counters
   float* P;   // rank-r split-K slabs
   float* Pm;  // main-GEMM split-K slabs
@@ -473,6 +478,8 @@ runlora_status_t bind_ws(const runlora_shape_t& s, void* ws, size_t ws_bytes, Bu
   char* base = static_cast<char*>(ws);
   b->z1 = base + L.z1;
   b->z2 = base + L.z2;
+  b->arep = base + L.arep;
+  b->brep = base + L.brep;
   b->cnt = reinterpret_cast<int*>(base + L.cnt);
   b->wp = base + L.wp;
   b->P = reinterpret_cast<float*>(base + L.p);
@@ -737,9 +744,10 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
     const ZPlan f = plan_z(s);
     if (f.ok && f.szf > 1) {
       // Z2 as szf K-split bf16 blocks (every CTA slot streams X, no reducer), then
-      // Y = [X | Z2_0 | .. | Z2_{szf-1}]·[W ; B ; .. ; B]: the tail repeats B itself per block
-      // (Prob::tail_rep), no stacked copy of B
+      // Y = [X | Z2_0 | .. | Z2_{szf-1}]·[W ; B ; .. ; B]: B stacked szf times (one 64-wide
+      // tail k-block), written by the Z2 launch's idle warps
       const int zc = (int)(r * f.szf);
+      const ReduceJob rep = repeat_job(B, 1, (int)(r * m), f.szf, b.brep);
       GemmReq z = base_req((int)n, (int)r, KID_GEMM_PROJ);
       z.a = mat(X, n, k);
       z.b = mat(A, k, r);
@@ -753,12 +761,12 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
       z.split_stride = r;
       z.splits = f.szf;
       z.kb_per_split = f.kpzf;
+      z.side = &rep;
+      z.nside = 1;
       RL_TRY(gemm(c, z, st));
       q.a2 = mat(b.z2, n, zc);
-      q.b2 = mat(B, r, m);
-      q.K2 = (int)r;
-      q.tail_rep = f.szf;
-      q.tail_w = (int)r;
+      q.b2 = mat(b.brep, zc, m);
+      q.K2 = zc;
     } else {
       Skinny j = job_Z2(s, X, A, b.z2);
       RL_TRY(run_skinny(c, &j, 1, b.P, b.cnt, KID_GEMM_PROJ, st));
@@ -779,7 +787,7 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
 // slabs are summed in fixed order either by the reductions launch itself (the last split per
 // output tile, Prob::fixup) or, with `defer`, by the idle warps of the dX GEMM launch that
 // follows (no reducer launch either way; see ZPlan).
-runlora_status_t grads_tok_bf16(Ctx& c, const ZPlan& f, const runlora_shape_t& s, const void* X, const void* A,
+runlora_status_t grads_tok_bf16(Ctx& c, int v, const ZPlan& f, const runlora_shape_t& s, const void* X, const void* A,
                                 const void* B, const void* dY, void* dA, void* dB, bool gb, bool acc, Bufs& b,
                                 cudaStream_t st, std::vector<ReduceJob>* defer) {
   const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
@@ -811,6 +819,12 @@ runlora_status_t grads_tok_bf16(Ctx& c, const ZPlan& f, const runlora_shape_t& s
   if (!defer) {
     q[0].zero_ptr = b.cnt;
     q[0].zero_n = tiles[0] + tiles[1];
+  }
+  // backward1's dX tail needs A repeated per Z1 block: written by this launch's idle warps
+  const ReduceJob rep = repeat_job(A, (int)k, (int)r, f.sz, b.arep);
+  if (v == 1 && f.sz > 1) {
+    q[0].side = &rep;
+    q[0].nside = 1;
   }
   cudaError_t e = launch_tc_gemm(c, q, 2, st, &err);
   if (e != cudaSuccess) return fail(RUNLORA_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
@@ -868,7 +882,7 @@ runlora_status_t params_bf16(Ctx& c, int v, const runlora_shape_t& s, const void
   const int64_t n = s.n, k = s.k, m = s.m;
   if (v == 1 || v == 5) {  // Alg. 1 / Alg. 5: Z1, Z2 | dA = Xᵀ·Z1, dB = Z2ᵀ·dY
     const ZPlan f = plan_z(s);
-    if (f.ok) return grads_tok_bf16(c, f, s, X, A, B, dY, dA, dB, gb, acc, b, st, defer);
+    if (f.ok) return grads_tok_bf16(c, v, f, s, X, A, B, dY, dA, dB, gb, acc, b, st, defer);
     Skinny pj[2] = {job_Z1(s, dY, B, b.z1), job_Z2(s, X, A, b.z2)};
     RL_TRY(run_skinny(c, pj, 2, b.P, b.cnt, KID_GEMM_PROJ, st));
     Skinny tj[2] = {job_dA_tok(s, X, b.z1, dA, gb, acc), job_dB_tok(s, dY, b.z2, dB, gb, acc)};
@@ -925,11 +939,11 @@ runlora_status_t input_bf16(Ctx& c, int v, const runlora_shape_t& s, const void*
     const ZPlan f = plan_z(s);
     if (v == 1 && f.ok && f.sz > 1) {
       // backward1's adapter-gradient pass left Z1 as sz partial blocks: dY·Wᵀ + Σ_s Z1_s·Aᵀ =
-      // [dY | Z1_0 | .. | Z1_{sz-1}]·[Wᵀ ; Aᵀ ; .. ; Aᵀ], the tail repeating A itself per
-      // block (Prob::tail_rep)
-      q.a2 = mat(b.z1, n, (int64_t)r * f.sz);
-      q.tail_rep = f.sz;
-      q.tail_w = (int)r;
+      // [dY | Z1_0 | .. | Z1_{sz-1}]·[Wᵀ ; Aᵀ ; .. ; Aᵀ] (A repeated by the projection launch)
+      const int zc = (int)(r * f.sz);
+      q.a2 = mat(b.z1, n, zc);
+      q.b2 = mat(b.arep, k, zc);
+      q.K2 = zc;
     }
   } else {  // dX = dY·W'ᵀ
     if (qw) RL_TRY(wprime_q(c, s, *qw, A, B, b.wp, false, true, st));  // W' [k, m] from Wq
@@ -1114,9 +1128,10 @@ runlora_status_t do_backward(runlora_handle_t h, int bwd, const runlora_shape_t*
   // adapter gradients, then dX — one PDL chain.  With dX, the adapter gradients' split-K slabs
   // are reduced (fixed order) by the idle warps 2-3 of the dX GEMM launch, concurrently with
   // its mainloop; without dX (or in the split _params call) their own launch reduces them.
+  static const bool side_ok = !getenv("RUNLORA_SIDE_REDUCE") || atoi(getenv("RUNLORA_SIDE_REDUCE")) != 0;
   std::vector<ReduceJob> side;
   RL_TRY(do_params(h, bwd, s, X, W, A, B, dY, dA, dB, grad_dtype, accumulate, ws, ws_bytes, stream,
-                   dX && s->dtype == RUNLORA_BF16 ? &side : nullptr));
+                   side_ok && dX && s->dtype == RUNLORA_BF16 ? &side : nullptr));
   if (dX) RL_TRY(do_input(h, bwd, s, W, A, B, dY, dX, ws, ws_bytes, stream, &side));
   return RUNLORA_OK;
 }

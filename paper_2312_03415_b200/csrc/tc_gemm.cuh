@@ -77,12 +77,12 @@ struct Prob {
   // B2 that belong to this tile's own M range.  D += I·B2[m0.., n0..] adds a matrix that is
   // indexed like the output (W + A·B: the add rides in the mainloop, exact in fp32).
   int tail_diag;
-  // Repeated concat-K tail: nk2 = tail_rep k-blocks, block s multiplies columns
-  // [s*tail_w, (s+1)*tail_w) of A2 with columns [0, tail_w) of the SAME B2 (e.g. Σ_s Z1_s·Aᵀ
-  // over the K-split partial blocks of Z1 against A itself, no repeated copy of A).  The MMA
-  // issues ⌈tail_w/16⌉ K-steps; A2 columns past tail_w inside a step meet B2's zero-filled
-  // (out-of-bounds) K rows.  0 = a plain tail.
-  int tail_rep, tail_w;
+};
+
+// Per-problem fields of the features added after the main GEMM was tuned, kept in their own
+// array at the END of GemmArgs so that the kernel parameter offsets the main GEMMs' hot loops
+// read stay where they were.
+struct ProbX {
   // Split-K fix-up (fp32 slab modes): the last split of an output tile to finish sums the
   // num_splits slabs of that tile in split order (deterministic) and writes
   //   out[i, c] (or out[c, i] when fx_transpose) {=, +=} sum_s slab[s][i][c],  c < fx_cols,
@@ -115,12 +115,11 @@ struct SideJob {
   long long split_stride, ldp, ldo;
   void* out;
   int splits, rows, cols, out_bf16, transpose, accumulate;
+  int repeat;  // > 0: column repeat of a bf16 matrix instead (dst[i, t*cols + j] = src[i, j], t < repeat)
 };
 
 struct GemmArgs {
   Prob p[kMaxProb];
-  SideJob side[2];
-  int nside;
   int nprob;
   int total_units;
   int dbg;  // 0 normal; 1: no TMA (MMA-only); 2: no MMA (TMA-only); 3: as 1 + no stores; 4: as 1 + no epilogue;
@@ -133,6 +132,9 @@ struct GemmArgs {
   int stages;                  // pipeline stages (0: the compiled maximum TileCfg::STAGES)
   int* zero_ptr;               // zeroed by CTA 0 after the PDL wait (split fix-up counters of a
   int zero_n;                  // later launch in the stream), nullptr: none
+  SideJob side[2];
+  int nside;
+  ProbX px[kMaxProb];
 };
 
 struct Tmaps {  // per problem: A1, B1, A2, B2, D (EPI = 3: TMA-store epilogue)
@@ -164,8 +166,9 @@ struct TileCfg {
   static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = (2 * BN_MAX <= 32) ? 32 : (2 * BN_MAX <= 64) ? 64
                                         : (2 * BN_MAX <= 128) ? 128 : (2 * BN_MAX <= 256) ? 256 : 512;
+  static constexpr bool FIXUP = CG == 1 && EPI == 0;  // kernels that compile the split fix-up
   static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + STG_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
-                                         4 * kMaxFixups /*split fix-up list*/;
+                                         (FIXUP ? 4 * kMaxFixups : 0) /*split fix-up list*/;
 };
 
 struct Unit {
@@ -273,12 +276,12 @@ __device__ __forceinline__ void store_row_segment(const Prob& p, int split, int 
 // the CTA whose split arrived last (Prob::fixup), after its unit loop.  Thread = row; 16-column
 // chunks; the slabs are summed in split order (deterministic), two splits' loads (8 x 16 B)
 // in flight before any is added.
-__device__ __forceinline__ void split_fixup(const Prob& p, int row, int n_blk) {
+__device__ __forceinline__ void split_fixup(const Prob& p, const ProbX& px, int row, int n_blk) {
   if (row >= p.M) return;
-  const int c_lo = n_blk * p.bn, c_hi = min(p.fx_cols, c_lo + p.bn);
+  const int c_lo = n_blk * p.bn, c_hi = min(px.fx_cols, c_lo + p.bn);
   const float* base = static_cast<const float*>(p.D) + (long long)row * p.ldd;
-  const long long ostep = p.fx_transpose ? p.fx_ldo : 1;
-  const long long obase = p.fx_transpose ? (long long)row : (long long)row * p.fx_ldo;
+  const long long ostep = px.fx_transpose ? px.fx_ldo : 1;
+  const long long obase = px.fx_transpose ? (long long)row : (long long)row * px.fx_ldo;
   const int S = p.num_splits;
 #pragma unroll 1
   for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
@@ -304,13 +307,13 @@ __device__ __forceinline__ void split_fixup(const Prob& p, int row, int n_blk) {
       if (c0 + e >= c_hi) break;
       const long long o = obase + (long long)(c0 + e) * ostep;
       float val = a[e];
-      if (p.fx_bf16) {
-        __nv_bfloat16* d = static_cast<__nv_bfloat16*>(p.fx_out) + o;
-        if (p.fx_accumulate) val += __bfloat162float(*d);
+      if (px.fx_bf16) {
+        __nv_bfloat16* d = static_cast<__nv_bfloat16*>(px.fx_out) + o;
+        if (px.fx_accumulate) val += __bfloat162float(*d);
         *d = __float2bfloat16_rn(val);
       } else {
-        float* d = static_cast<float*>(p.fx_out) + o;
-        if (p.fx_accumulate) val += *d;
+        float* d = static_cast<float*>(px.fx_out) + o;
+        if (px.fx_accumulate) val += *d;
         *d = val;
       }
     }
@@ -324,6 +327,17 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: 
 __device__ __forceinline__ void side_reduce(const GemmArgs& g, long long tid, long long nthr) {
   for (int j = 0; j < g.nside; ++j) {
     const SideJob& J = g.side[j];
+    if (J.repeat > 0) {  // bf16 column repeat, 16-byte groups
+      const int gc = J.cols >> 3;
+      const long long total = (long long)J.rows * gc * J.repeat;
+      const uint4* src = reinterpret_cast<const uint4*>(J.P);
+      uint4* dst = static_cast<uint4*>(J.out);
+      for (long long idx = tid; idx < total; idx += nthr) {
+        const long long i = idx / ((long long)gc * J.repeat);
+        dst[idx] = src[i * gc + (int)(idx % gc)];
+      }
+      continue;
+    }
     const int groups = (J.cols + 3) >> 2;
     const long long total = (long long)J.rows * groups;
     for (long long idx = tid; idx < total; idx += nthr) {
@@ -421,6 +435,12 @@ template <int BN_MAX, int CG, int OCC = 1, int EPI = 0, int KS = 1>
 __global__ void __launch_bounds__(kGemmThreads, OCC)
     tc_gemm_kernel(const __grid_constant__ Tmaps tm, const __grid_constant__ GemmArgs g) {
   using C = TileCfg<BN_MAX, CG, OCC, EPI, KS>;
+  // features compiled only where they are used, so the main GEMMs' code (and its MMA issue
+  // loop) stays as lean as before them: the FP8 identity tail and its scaling epilogue (W'
+  // builds from a quantized W: single-CTA TMA-store kernel), the split fix-up (rank-r kernels)
+  constexpr bool kFp8Tail = CG == 1 && EPI == 3;
+  constexpr bool kFixup = C::FIXUP;
+  constexpr bool kSide = KS == 1;  // side jobs ride on K-major launches (dX GEMM, projections)
   // runtime ring depth <= the compiled maximum (fewer stages leave shared memory to kernels
   // that should co-reside, e.g. NCCL's during an overlapped allreduce)
   const int STAGES = (g.stages > 0 && g.stages < C::STAGES) ? g.stages : C::STAGES;
@@ -497,6 +517,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       if (u < 0) break;
       const Unit t = decode_unit(g, u);
       const Prob& p = g.p[t.prob];
+      const ProbX& px = g.px[t.prob];
       if (g.trace && lane == 0) {
         g.trace[8 * u + 0] = globaltimer();
         g.trace[8 * u + 4] = blockIdx.x;
@@ -510,6 +531,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       const int kb1 = min(p.nk1, kb0 + p.kb_per_split);
       const int nmain = kb1 - kb0;
       const int nkb = nmain + (t.split == 0 ? p.nk2 : 0);
+      const bool fp8_tail = kFp8Tail && px.tail_fp8;
       // snake: every other round of this CTA walks K backwards, starting where the data it
       // (and its neighbours) just streamed is still in L2
       const bool rev = p.snake && (i_u & 1);
@@ -539,10 +561,12 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
             // K coordinates of the A and B boxes: main k-block, plain tail block, repeated
             // tail block (A2 column block s against B2 from K = 0), identity tail (B2 rows of
             // this tile)
-            const int kc = !tail ? (kb0 + ki) * kBK : p.tail_rep ? (i - nmain) * p.tail_w : (i - nmain) * kBK;
+            // (this loop sets the 256-wide kernels' TMA issue rate: one more parameter-dependent
+            // select per atom here measured 5-8 % slower main GEMMs)
+            const int kc = (tail ? (i - nmain) : (kb0 + ki)) * kBK;
             const int ma = diag ? 0 : m0;          // identity tail: rows of I
-            const int kcb = diag ? m0 + kc : (tail && p.tail_rep) ? 0 : kc;
-            if (tail && p.tail_fp8) {
+            const int kcb = diag ? m0 + kc : kc;   // identity tail: B2 rows of this tile
+            if (fp8_tail && tail) {
               // the 128x128 E4M3 identity and this tile's 128 Wq rows (one 128-byte K row each):
               // K-major B2 is Wq[n0.., m0..] (x = K = m0), MN-major B2 is Wq[m0.., n0..] (x = N)
               tma_load_2d<CG>(ta, fb, a, 0, 0, p.hint_a);
@@ -597,6 +621,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       if (u < 0) break;
       const Unit t = decode_unit(g, u);
       const Prob& p = g.p[t.prob];
+      const ProbX& px = g.px[t.prob];
       const int kb0 = t.split * p.kb_per_split;
       const int kb1 = min(p.nk1, kb0 + p.kb_per_split);
       const int nmain = kb1 - kb0;
@@ -605,6 +630,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       // (and its neighbours) just streamed is still in L2
       const bool rev = p.snake && (it & 1);
       const int nh = BN_MAX > SLOT_W ? unit_halves(p, t.n_blk, SLOT_W) : 1;
+      const bool fp8_tail = kFp8Tail && px.tail_fp8;
       const int s0 = sc & 1;
       mbar_wait(&tempty[s0], ((s0 ? use1 : use0) & 1) ^ 1);
       tc_fence_after();
@@ -621,13 +647,11 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
         for (int at = 0; at < natoms; ++at) {
           const int i = i0 + at;
           const int ki = rev ? nmain - 1 - i : i;
-          const int kleft = (i < nmain)   ? (p.k1 - (kb0 + ki) * kBK)
-                            : p.tail_rep ? p.tail_w
-                                         : (p.k2 - (i - nmain) * kBK);
+          const int kleft = (i < nmain) ? (p.k1 - (kb0 + ki) * kBK) : (p.k2 - (i - nmain) * kBK);
           const int ksteps = min(kBK / 16, (kleft + 15) >> 4);
           const uint32_t a_addr = smem_u32(sA + st * C::A_BYTES + at * C::A_ATOM);
           const uint32_t b_addr = smem_u32(sB + st * C::B_BYTES + at * C::B_ATOM);
-          if (i >= nmain && p.tail_fp8) {
+          if (fp8_tail && i >= nmain) {
             // 4 K-steps of 32 E4M3 elements (32 B along a K-major row, 32 rows = 4 KB of an
             // MN-major tile) into the second accumulator at column bn; the first step starts it
             const uint64_t a8 = smem_desc(0, p.a_mn ? 16384u : 16u, 1024u, 2u);
@@ -635,7 +659,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
             const uint32_t as = p.a_mn ? 4096u : 32u, bs = p.b_mn ? 4096u : 32u;
             for (int j = 0; j < 4; ++j)
               umma_f8(d_tmem + (uint32_t)p.bn, a8 | (uint64_t)(((a_addr + j * as) >> 4) & 0x3FFF),
-                      b8 | (uint64_t)(((b_addr + j * bs) >> 4) & 0x3FFF), p.idesc2, j > 0 ? 1u : 0u);
+                      b8 | (uint64_t)(((b_addr + j * bs) >> 4) & 0x3FFF), px.idesc2, j > 0 ? 1u : 0u);
             continue;
           }
           for (int j = 0; j < (g.dbg == 2 ? 0 : ksteps); ++j) {
@@ -708,7 +732,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       }
       sc += nh;
     }
-  } else if ((warp == 2 || warp == 3) && g.nside > 0) {
+  } else if (kSide && (warp == 2 || warp == 3) && g.nside > 0) {
     // ----------------------------------------------- side job of the idle warps
     side_reduce(g, (long long)blockIdx.x * 64 + (threadIdx.x - 64), (long long)gridDim.x * 64);
   } else if (warp >= 4) {
@@ -723,6 +747,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       if (u < 0) break;
       const Unit t = decode_unit(g, u);
       const Prob& p = g.p[t.prob];
+      const ProbX& px = g.px[t.prob];
       const int m0 = t.m_blk * (kBM * CG) + rank * kBM;
       const int n0 = t.n_blk * p.bn;
       const int row = (g.dbg == 3) ? 0x7fffffff : m0 + q * 32 + lane;
@@ -798,9 +823,9 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
           uint8_t* stg = smem + STAGES * C::STAGE_BYTES + q * (C::STG_BUFS * 4096);
           const int nch = min(bw, p.N - nc + 63) / 64;  // 64-column chunks inside N
           const CUtensorMap* dmap = &tm.m[t.prob][4];
-          if (p.out_mode == OUT_BF16_WQ) {
+          if (kFp8Tail && p.out_mode == OUT_BF16_WQ) {
             // D = bf16(acc + bf16(acc_q · scale)); acc_q at slot column bn (Prob::tail_fp8)
-            const float srow = (p.wq_row_scale && row < p.M) ? __ldg(p.wq_scale + row) : 0.f;
+            const float srow = (px.wq_row_scale && row < p.M) ? __ldg(px.wq_scale + row) : 0.f;
 #pragma unroll 1
             for (int i = 0; i < nch; ++i) {
               uint32_t pk[32];
@@ -814,25 +839,31 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
                 reg_fence32(vq);
                 if (p.nk1 > 0) reg_fence32(va);
                 float sc[32];
-                if (p.wq_row_scale) {
+                if (px.wq_row_scale) {
 #pragma unroll
                   for (int x = 0; x < 32; ++x) sc[x] = srow;
                 } else {
 #pragma unroll
                   for (int x = 0; x < 32; x += 4) {
                     const int col = nc + cc + x;
-                    const float4 s4 = col < p.N ? __ldg(reinterpret_cast<const float4*>(p.wq_scale + col))
+                    const float4 s4 = col < p.N ? __ldg(reinterpret_cast<const float4*>(px.wq_scale + col))
                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
                     sc[x] = s4.x, sc[x + 1] = s4.y, sc[x + 2] = s4.z, sc[x + 3] = s4.w;
                   }
                 }
 #pragma unroll
                 for (int x = 0; x < 32; x += 2) {
-                  // W~ = bf16(e4m3 · scale) (R18), then + the fp32 A·B, one rounding
-                  float w0 = __bfloat162float(__float2bfloat16_rn(__uint_as_float(vq[x]) * sc[x]));
-                  float w1 = __bfloat162float(__float2bfloat16_rn(__uint_as_float(vq[x + 1]) * sc[x + 1]));
-                  if (p.nk1 > 0) w0 += __uint_as_float(va[x]), w1 += __uint_as_float(va[x + 1]);
-                  pk[16 * hh + x / 2] = pack_bf16x2(w0, w1);
+                  // W~ = bf16(e4m3 · scale) (R18) for a pair in ONE packed conversion (the single
+                  // float->bf16 conversion runs on the quarter-rate XU pipe), then + the fp32 A·B
+                  // and one rounding
+                  const uint32_t w2 = pack_bf16x2(__uint_as_float(vq[x]) * sc[x], __uint_as_float(vq[x + 1]) * sc[x + 1]);
+                  if (p.nk1 > 0) {
+                    const float w0 = __uint_as_float(w2 << 16) + __uint_as_float(va[x]);
+                    const float w1 = __uint_as_float(w2 & 0xFFFF0000u) + __uint_as_float(va[x + 1]);
+                    pk[16 * hh + x / 2] = pack_bf16x2(w0, w1);
+                  } else {
+                    pk[16 * hh + x / 2] = w2;
+                  }
                 }
               }
               stage_store_packed<C::STG_BUFS>(pk, stg, st_it, lane, dmap, nc + 64 * i, m0 + q * 32);
@@ -912,13 +943,13 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
         else ++use0;
       }
       sc += nh;
-      if (p.fixup) {
+      if (kFixup && px.fixup) {
         // split-K fix-up: count this split's arrival at its output tile once all 128 rows of
         // the slab are stored; the last split to arrive reduces the tile (after the loop)
         __threadfence();
         epi_bar();
         if (threadIdx.x == 4 * 32 &&
-            atomicAdd(&p.counters[t.m_blk * p.num_n_tiles + t.n_blk], 1) == p.num_splits - 1)
+            atomicAdd(&px.counters[t.m_blk * p.num_n_tiles + t.n_blk], 1) == p.num_splits - 1)
           fx_list[(*fx_count)++] = (t.prob << 24) | (t.n_blk << 16) | t.m_blk;
       }
       if (g.trace && threadIdx.x == 4 * 32) g.trace[8 * u + 3] = globaltimer();
@@ -927,7 +958,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       if (lane == 0) bulk_wait_all();  // stores complete before the CTA retires
       __syncwarp();
     }
-    if constexpr (EPI != 3) {
+    if constexpr (kFixup) {
       epi_bar();
       const int nfx = *fx_count;
       if (nfx > 0) {
@@ -935,8 +966,9 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
         for (int f = 0; f < nfx; ++f) {
           const int e = fx_list[f];
           const Prob& p = g.p[e >> 24];
+          const ProbX& px = g.px[e >> 24];
           const int m_blk = e & 0xFFFF, n_blk = (e >> 16) & 0xFF;
-          split_fixup(p, m_blk * kBM + q * 32 + lane, n_blk);
+          split_fixup(p, px, m_blk * kBM + q * 32 + lane, n_blk);
         }
       }
     }
