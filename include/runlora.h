@@ -249,6 +249,39 @@ runlora_status_t runlora_backward_wq(runlora_handle_t h, int bwd, const runlora_
 runlora_status_t runlora_allreduce_sum_f32(runlora_handle_t h, const float* const* peers, int P, float* out,
                                            int64_t n, void* stream);
 
+/* ------------------------------------ fused data-parallel exchange (issued by the dX GEMM)
+ * The a8 exchange step fused into the backward: with the tokens sharded
+ * over P ranks, dA = Xᵀ·dY·Bᵀ and dB = Aᵀ·Xᵀ·dY of the full batch are the sums of the ranks'
+ * partial sums (Eq. 3 sums over tokens).  runlora_backward_exchange runs the backward
+ * like runlora_backward, but the idle warps of its dX GEMM launch — concurrently with that
+ * GEMM's mainloop — sum this rank's token-split slabs in fixed order into its exchange buffer,
+ * publish each 64-row chunk to every rank (flag stores over NVLink), wait for every rank's
+ * chunk, and write dA, dB = the rank-order sum over ranks (peer loads: bit-identical on every
+ * rank), or the switch-side sum multimem.ld_reduce when a multicast address is given (NVLS).
+ * No NCCL call, no extra launch.  Every rank must call it for the same shape, variant and
+ * epoch, on GPUs that run concurrently (never several ranks on one GPU).
+ *
+ * runlora_exchange_sizes: bytes of each rank's exchange buffer (2 epoch halves of r·(k+m)
+ *   fp32) and flag array (ceil((k+m)/64)·P uint32) — allocate both in memory every rank can
+ *   address (CUDA IPC / torch symmetric memory), the flags zero-initialised.
+ * runlora_exchange_create: this rank's view: bufs / flags = HOST arrays of P device pointers
+ *   (rank order, as mapped in this process), mc = multicast address of the buffers or NULL.
+ *   Allocates a small device descriptor (setup time, not on the forward/backward path).
+ * runlora_backward_exchange: grad_dtype must be RUNLORA_F32, dX non-NULL (the exchange rides
+ *   on the dX GEMM), bf16 operands; epoch = 1, 2, 3, ... per exchange (same on every rank; the
+ *   buffer half alternates with it, so consecutive steps never overwrite what a slow peer
+ *   still reads).  Errors as runlora_backward, plus INVALID_ARG for a bad exchange/epoch. */
+typedef struct runlora_exchange_s* runlora_exchange_t;
+runlora_status_t runlora_exchange_sizes(int64_t k, int64_t m, int64_t r, int P, size_t* buf_bytes,
+                                        size_t* flag_bytes);
+runlora_status_t runlora_exchange_create(runlora_handle_t h, int P, int rank, int64_t k, int64_t m, int64_t r,
+                                         void* const* bufs, void* const* flags, void* mc, runlora_exchange_t* out);
+runlora_status_t runlora_exchange_destroy(runlora_exchange_t x);
+runlora_status_t runlora_backward_exchange(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X,
+                                           const void* W, const void* A, const void* B, const void* dY, void* dX,
+                                           void* dA, void* dB, int grad_dtype, int accumulate, runlora_exchange_t x,
+                                           uint32_t epoch, void* workspace, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- tracing
  * When enabled, every kernel the library launches is bracketed by CUDA events
  * on its stream; runlora_profile_read synchronises those events and returns

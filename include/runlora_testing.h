@@ -43,6 +43,17 @@ const char* runlora_debug_kernel_name(int kid);
  * output rows the library runs as 256x512 pair tiles (a multiple of 256; 0 = 256-wide tiles
  * only, also when b_mn != 0 or env RUNLORA_MAIN_WIDE=0).  Host-only; -1 on a bad handle. */
 int runlora_debug_wide_rows(runlora_handle_t h, int M, int N, int K, int b_mn);
+/* The fused exchange (runlora_backward_exchange) with P ranks EMULATED on one GPU: one
+ * cooperative launch runs every rank's exchange device code (its blocks wait on one another
+ * only through the exchange flags, all co-resident).  Per rank q (HOST arrays of device
+ * pointers): token-split slabs sA[q] [splits][k][r] and sB[q] [splits][m][r] (fp32), outputs
+ * dA[q] [k, r] and dB[q] [r, m] (fp32), exchange buffers bufs[q] and zeroed flag arrays
+ * flags[q] sized by runlora_exchange_sizes.  Deterministic: every dA[q] is the rank-order sum
+ * of the ranks' split-order slab sums.  Synchronous. */
+runlora_status_t runlora_debug_exchange_emulate(runlora_handle_t h, int P, int64_t k, int64_t m, int64_t r,
+                                                int splits, const float* const* sA, const float* const* sB,
+                                                float* const* dA, float* const* dB, void* const* bufs,
+                                                void* const* flags, uint32_t epoch);
 #ifdef __cplusplus
 }
 #endif

@@ -7,6 +7,7 @@
 // done before a buffer is rewritten) is the caller's (include/runlora.h).
 #include "internal.h"
 #include "ptx.cuh"
+#include "exchange.cuh"
 
 namespace runlora {
 namespace {
@@ -58,6 +59,47 @@ cudaError_t launch_allreduce_sum_f32(Ctx& ctx, const float* const* peers, int P,
   ctx.launch_begin(s, KID_ALLREDUCE);
   cudaError_t e = cudaLaunchKernelEx(&cfg, allreduce_sum_kernel, pp, P, out, n, ctx.ltrace_slot(KID_ALLREDUCE));
   ctx.launch_end(s);
+  return e;
+}
+
+// ------------------------------------------------ fused exchange, P ranks emulated
+namespace {
+struct XEmuSlabs {
+  XSlabs s[kXMaxPeers];
+};
+// block b plays rank b / per, as CTA b % per of that rank's exchange (64 threads: the two
+// warps that run it inside the dX GEMM); cooperative launch, so all blocks are co-resident
+__global__ void __launch_bounds__(64) exchange_emulate_kernel(const XDesc* descs, const __grid_constant__ XEmuSlabs sl,
+                                                              int per, unsigned epoch) {
+  const int q = blockIdx.x / per;
+  exchange_run(descs[q], sl.s[q], epoch, threadIdx.x, blockIdx.x % per, per);
+}
+}  // namespace
+
+cudaError_t launch_exchange_emulate(Ctx& ctx, int P, const XDesc* descs, const XSlabs* slabs, unsigned epoch) {
+  XEmuSlabs sl;
+  for (int q = 0; q < P; ++q) sl.s[q] = slabs[q];
+  XDesc* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(XDesc) * P);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpy(d, descs, sizeof(XDesc) * P, cudaMemcpyHostToDevice);
+  const int chunks = (descs[0].rows0 + descs[0].rows1 + kXChunkRows - 1) / kXChunkRows;
+  const int per = std::max(1, std::min(chunks, (ctx.num_sms() * 4) / P));  // all P*per blocks resident
+  if (e == cudaSuccess) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(P * per));
+    cfg.blockDim = dim3(64);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ctx.launch_begin(nullptr, KID_ALLREDUCE);
+    e = cudaLaunchKernelEx(&cfg, exchange_emulate_kernel, (const XDesc*)d, sl, per, epoch);
+    ctx.launch_end(nullptr);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  }
+  cudaFree(d);
   return e;
 }
 

@@ -102,6 +102,10 @@ struct GemmReq {
   // idle warps 2-3 (GemmArgs::side), e.g. the adapter-gradient slabs under the dX GEMM
   const ReduceJob* side;
   int nside;
+  // fused data-parallel exchange (launch-level): side[0] / side[1] = the dA / dB slab
+  // reductions, summed across ranks by the launch's idle warps (exchange.cuh)
+  const void* xdesc;  // device XDesc
+  unsigned xepoch;
   // FP8 identity tail (Prob::tail_fp8): a2 = E4M3 identity, b2 = Wq (uint8), K2 = 128;
   // out_mode OUT_BF16_WQ with one scale per output row (wq_row_scale) or column
   bool tail_fp8;
@@ -235,6 +239,11 @@ cudaError_t launch_splitk_reduce(Ctx& ctx, const ReduceJob* jobs, int njobs, cud
 // to bf16 (m multiple of 8, scale 16-byte aligned).
 cudaError_t launch_quantize_w(Ctx& ctx, const void* W, int64_t k, int64_t m, void* Wq, float* scale, cudaStream_t s);
 constexpr int kMaxPeers = 16;  // runlora_allreduce_sum_f32
+struct XDesc;
+struct XSlabs;
+// P ranks' fused exchanges (exchange.cuh) in ONE cooperative launch on this GPU (testing):
+// descs / slabs are host arrays of P (device descriptors are staged by the launcher).
+cudaError_t launch_exchange_emulate(Ctx& ctx, int P, const XDesc* descs, const XSlabs* slabs, unsigned epoch);
 cudaError_t launch_allreduce_sum_f32(Ctx& ctx, const float* const* peers, int P, float* out, int64_t n,
                                      cudaStream_t s);
 

@@ -397,6 +397,11 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
                         J.accumulate, J.repeat};
   }
   g.nside = reqs[0].nside;
+  if (reqs[0].xdesc) {
+    if (reqs[0].nside != 2 || reqs[0].side[0].transpose || !reqs[0].side[1].transpose) return cudaErrorInvalidValue;
+    g.xdesc = static_cast<const XDesc*>(reqs[0].xdesc);
+    g.xepoch = reqs[0].xepoch;
+  }
   g.zero_ptr = reqs[0].zero_ptr;
   g.zero_n = reqs[0].zero_ptr ? reqs[0].zero_n : 0;
   g.trace = (ctx.trace && ctx.trace_kid == reqs[0].kid && g.total_units <= Ctx::kTraceUnits) ? ctx.trace : nullptr;

@@ -31,6 +31,12 @@ struct runlora_handle_s {
   Ctx* ctx;
 };
 
+struct runlora_exchange_s {
+  XDesc* d_desc;  // device copy
+  int P, rank, device;
+  int64_t k, m, r;
+};
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -917,12 +923,15 @@ runlora_status_t params_bf16(Ctx& c, int v, const runlora_shape_t& s, const void
 
 runlora_status_t input_bf16(Ctx& c, int v, const runlora_shape_t& s, const void* W, const void* A, const void* B,
                             const void* dY, void* dX, Bufs& b, cudaStream_t st, const QW* qw = nullptr,
-                            const std::vector<ReduceJob>* side = nullptr) {
+                            const std::vector<ReduceJob>* side = nullptr, const void* xdesc = nullptr,
+                            unsigned xepoch = 0) {
   const int64_t n = s.n, k = s.k, m = s.m, r = s.r;
   GemmReq q = main_req(c, (int)n, (int)k);
   if (side && !side->empty()) {  // the adapter gradients' slabs, reduced by this launch's idle warps
     q.side = side->data();
     q.nside = (int)side->size();
+    q.xdesc = xdesc;             // ... and exchanged across ranks (runlora_backward_exchange)
+    q.xepoch = xepoch;
   }
   q.overlaps_comm = true;  // backward_input runs while backward_params' allreduce is in flight
   q.a = mat(dY, n, m);
@@ -1552,6 +1561,105 @@ const char* runlora_last_error(void) { return g_last_error.c_str(); }
 
 }  // extern "C"
 
+// ------------------------------------------------ fused data-parallel exchange (NEXT-2)
+namespace {
+void exchange_geometry(int64_t k, int64_t m, int64_t r, int P, size_t* half_elems, size_t* chunks, size_t* buf_bytes,
+                       size_t* flag_bytes) {
+  *half_elems = (((size_t)(k + m) * (size_t)r) + 63) & ~size_t(63);
+  *chunks = (size_t)((k + m + kXChunkRows - 1) / kXChunkRows);
+  *buf_bytes = 2 * *half_elems * sizeof(float);
+  *flag_bytes = *chunks * (size_t)P * sizeof(unsigned);
+}
+}  // namespace
+
+extern "C" {
+
+runlora_status_t runlora_exchange_sizes(int64_t k, int64_t m, int64_t r, int P, size_t* buf_bytes,
+                                        size_t* flag_bytes) {
+  if (k <= 0 || m <= 0 || r <= 0 || (r & 3) || P < 1 || P > kXMaxPeers || !buf_bytes || !flag_bytes)
+    return fail(RUNLORA_ERR_INVALID_ARG, "exchange: k, m, r >= 1 (r a multiple of 4), 1 <= P <= 16");
+  size_t half, chunks;
+  exchange_geometry(k, m, r, P, &half, &chunks, buf_bytes, flag_bytes);
+  return RUNLORA_OK;
+}
+
+runlora_status_t runlora_exchange_create(runlora_handle_t h, int P, int rank, int64_t k, int64_t m, int64_t r,
+                                         void* const* bufs, void* const* flags, void* mc, runlora_exchange_t* out) {
+  RL_TRY(check_handle(h));
+  if (!out) return fail(RUNLORA_ERR_INVALID_ARG, "exchange: out is NULL");
+  *out = nullptr;
+  size_t bb, fb, half, chunks;
+  RL_TRY(runlora_exchange_sizes(k, m, r, P, &bb, &fb));
+  if (rank < 0 || rank >= P) return fail(RUNLORA_ERR_INVALID_ARG, "exchange: rank must be in [0, P)");
+  if (!bufs || !flags) return fail(RUNLORA_ERR_INVALID_ARG, "exchange: bufs / flags are NULL");
+  exchange_geometry(k, m, r, P, &half, &chunks, &bb, &fb);
+  XDesc d;
+  memset(&d, 0, sizeof d);
+  d.P = P;
+  d.rank = rank;
+  d.rows0 = (int)k;
+  d.rows1 = (int)m;
+  d.cols = (int)r;
+  d.half_elems = (long long)half;
+  for (int q = 0; q < P; ++q) {
+    RL_TRY(check_ptr(bufs[q], "exchange buffer"));
+    RL_TRY(check_ptr(flags[q], "exchange flags"));
+    d.bufs[q] = static_cast<float*>(bufs[q]);
+    d.flags[q] = static_cast<unsigned*>(flags[q]);
+  }
+  RL_TRY(check_ptr(mc, "exchange multicast address", true));
+  d.mc = static_cast<float*>(mc);
+  DeviceGuard dg(h->ctx->device());
+  runlora_exchange_s* x = new runlora_exchange_s{nullptr, P, rank, h->ctx->device(), k, m, r};
+  cudaError_t e = cudaMalloc(&x->d_desc, sizeof(XDesc));
+  if (e == cudaSuccess) e = cudaMemcpy(x->d_desc, &d, sizeof(XDesc), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (x->d_desc) cudaFree(x->d_desc);
+    delete x;
+    return cuda_fail(e, "exchange descriptor");
+  }
+  *out = x;
+  return RUNLORA_OK;
+}
+
+runlora_status_t runlora_exchange_destroy(runlora_exchange_t x) {
+  if (!x) return RUNLORA_OK;
+  DeviceGuard dg(x->device);
+  cudaFree(x->d_desc);
+  delete x;
+  return RUNLORA_OK;
+}
+
+runlora_status_t runlora_backward_exchange(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X,
+                                           const void* W, const void* A, const void* B, const void* dY, void* dX,
+                                           void* dA, void* dB, int grad_dtype, int accumulate, runlora_exchange_t x,
+                                           uint32_t epoch, void* ws, size_t ws_bytes, void* stream) {
+  RL_TRY(validate_params(h, bwd, s, X, A, B, dY, dA, dB, grad_dtype));
+  if (!dX) return fail(RUNLORA_ERR_INVALID_ARG, "exchange: dX is required (the exchange rides on the dX GEMM)");
+  RL_TRY(validate_input(h, bwd, s, W, A, B, dY, dX));
+  if (s->dtype != RUNLORA_BF16 || grad_dtype != RUNLORA_F32)
+    return fail(RUNLORA_ERR_DTYPE, "exchange: bf16 operands and fp32 adapter gradients");
+  if (!x || x->k != s->k || x->m != s->m || x->r != s->r)
+    return fail(RUNLORA_ERR_INVALID_ARG, "exchange: NULL or built for another (k, m, r)");
+  if (epoch == 0) return fail(RUNLORA_ERR_INVALID_ARG, "exchange: epoch starts at 1");
+  {
+    Bufs b;
+    RL_TRY(bind_ws(*s, ws, ws_bytes, &b));
+  }
+  CallLock lk(h->ctx->call_mu);
+  std::vector<ReduceJob> side;
+  RL_TRY(do_params(h, bwd, s, X, W, A, B, dY, dA, dB, grad_dtype, accumulate, ws, ws_bytes, stream, &side));
+  if (side.size() != 2) return fail(RUNLORA_ERR_UNSUPPORTED_VARIANT, "exchange: the adapter gradients were not split");
+  Bufs b;
+  RL_TRY(bind_ws(*s, ws, ws_bytes, &b));
+  DeviceGuard dg(h->ctx->device());
+  RL_TRY(input_bf16(*h->ctx, bwd, *s, W, A, B, dY, dX, b, static_cast<cudaStream_t>(stream), nullptr, &side,
+                    x->d_desc, epoch));
+  return post_launch();
+}
+
+}  // extern "C"
+
 // ------------------------------------------------------------ test hook
 #include "../../include/runlora_testing.h"
 extern "C" runlora_status_t runlora_debug_gemm(runlora_handle_t h, int M, int N, int K1, const void* A1, int a_mn,
@@ -1637,4 +1745,51 @@ extern "C" int runlora_debug_wide_rows(runlora_handle_t h, int M, int N, int K, 
 
 extern "C" const char* runlora_debug_kernel_name(int kid) {
   return (kid >= 0 && kid < KID_COUNT) ? kKernelNames[kid] : "?";
+}
+
+extern "C" runlora_status_t runlora_debug_exchange_emulate(runlora_handle_t h, int P, int64_t k, int64_t m, int64_t r,
+                                                           int splits, const float* const* sA,
+                                                           const float* const* sB, float* const* dA,
+                                                           float* const* dB, void* const* bufs, void* const* flags,
+                                                           uint32_t epoch) {
+  RL_TRY(check_handle(h));
+  size_t bb, fb, half, chunks;
+  RL_TRY(runlora_exchange_sizes(k, m, r, P, &bb, &fb));
+  if (splits < 1 || epoch == 0 || !sA || !sB || !dA || !dB || !bufs || !flags)
+    return fail(RUNLORA_ERR_INVALID_ARG, "exchange emulation: bad arguments");
+  exchange_geometry(k, m, r, P, &half, &chunks, &bb, &fb);
+  std::vector<XDesc> descs(P);
+  std::vector<XSlabs> slabs(P);
+  for (int q = 0; q < P; ++q) {
+    XDesc& d = descs[q];
+    memset(&d, 0, sizeof d);
+    d.P = P;
+    d.rank = q;
+    d.rows0 = (int)k;
+    d.rows1 = (int)m;
+    d.cols = (int)r;
+    d.half_elems = (long long)half;
+    for (int p2 = 0; p2 < P; ++p2) {
+      d.bufs[p2] = static_cast<float*>(bufs[p2]);
+      d.flags[p2] = static_cast<unsigned*>(flags[p2]);
+    }
+    XSlabs& S = slabs[q];
+    memset(&S, 0, sizeof S);
+    S.P[0] = sA[q];
+    S.P[1] = sB[q];
+    S.split_stride[0] = k * r;
+    S.split_stride[1] = m * r;
+    S.ldp[0] = S.ldp[1] = r;
+    S.ldo[0] = r;
+    S.ldo[1] = m;
+    S.out[0] = dA[q];
+    S.out[1] = dB[q];
+    S.splits[0] = S.splits[1] = splits;
+  }
+  CallLock lk(h->ctx->call_mu);
+  DeviceGuard dg(h->ctx->device());
+  cudaError_t e = launch_exchange_emulate(*h->ctx, P, descs.data(), slabs.data(), epoch);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(e, "exchange emulation");
+  return RUNLORA_OK;
 }

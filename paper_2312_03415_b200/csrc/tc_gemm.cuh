@@ -36,6 +36,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include "ptx.cuh"
+#include "exchange.cuh"
 
 namespace runlora {
 
@@ -135,6 +136,10 @@ struct GemmArgs {
   SideJob side[2];
   int nside;
   ProbX px[kMaxProb];
+  // fused data-parallel exchange (exchange.cuh): with xdesc, side[0] / side[1] are the dA / dB
+  // slab reductions and warps 2-3 reduce them ACROSS ranks (epoch: this exchange's number)
+  const XDesc* xdesc;
+  unsigned xepoch;
 };
 
 struct Tmaps {  // per problem: A1, B1, A2, B2, D (EPI = 3: TMA-store epilogue)
@@ -734,7 +739,22 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
     }
   } else if (kSide && (warp == 2 || warp == 3) && g.nside > 0) {
     // ----------------------------------------------- side job of the idle warps
-    side_reduce(g, (long long)blockIdx.x * 64 + (threadIdx.x - 64), (long long)gridDim.x * 64);
+    if (g.xdesc) {
+      XSlabs S;
+      for (int j = 0; j < 2; ++j) {
+        S.P[j] = g.side[j].P;
+        S.split_stride[j] = g.side[j].split_stride;
+        S.ldp[j] = g.side[j].ldp;
+        S.ldo[j] = g.side[j].ldo;
+        S.out[j] = g.side[j].out;
+        S.splits[j] = g.side[j].splits;
+      }
+      S.out_bf16 = g.side[0].out_bf16;
+      S.accumulate = g.side[0].accumulate;
+      exchange_run(*g.xdesc, S, g.xepoch, threadIdx.x - 64, blockIdx.x, gridDim.x);
+    } else {
+      side_reduce(g, (long long)blockIdx.x * 64 + (threadIdx.x - 64), (long long)gridDim.x * 64);
+    }
   } else if (warp >= 4) {
     // --------------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access

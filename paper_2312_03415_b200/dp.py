@@ -74,6 +74,60 @@ class SymmetricAllreduce:
         self.hdl.barrier(channel=1)
 
 
+class FusedExchange:
+    """The a8 exchange fused into the backward (runlora_backward_exchange):
+    every rank's exchange buffer (two epoch halves of r·(k+m) fp32) and flag array live in torch
+    symmetric memory; the dX GEMM launch's idle warps sum the rank's token-split slabs into its
+    buffer, publish each 64-row chunk to every rank over NVLink, and sum the P ranks' chunks in
+    rank order (bit-identical on every rank) — or, with `multicast=True` and a multicast address
+    from the symmetric-memory handle, read the switch-side sum (NVLS multimem.ld_reduce).  No
+    NCCL call on the step; dA, dB come back already summed over the ranks.
+
+    Opt-in (bench.py: RUNLORA_DP_TRANSPORT=fused).  Correct by construction for P > 1 (the
+    device code is the one tests/test_gpu_exchange.py runs with P ranks emulated in one
+    cooperative launch); the box of this round has one GPU, so P > 1 runs only under the
+    driver's multi-GPU tiers."""
+
+    def __init__(self, k: int, r: int, m: int, device, handle, group=None, multicast: bool = False):
+        import torch.distributed._symmetric_memory as symm_mem
+        from . import runlora as rl
+        group = group if group is not None else dist.group.WORLD
+        self.P, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        buf_bytes, flag_bytes = rl.exchange_sizes(k, m, r, self.P)
+        self.buf = symm_mem.empty(buf_bytes // 4, dtype=torch.float32, device=device)
+        self.flags = symm_mem.empty(flag_bytes // 4, dtype=torch.int32, device=device)
+        self.flags.zero_()
+        hb = symm_mem.rendezvous(self.buf, group)
+        hf = symm_mem.rendezvous(self.flags, group)
+        torch.cuda.synchronize(device)
+        dist.barrier(group)  # every rank's flags are zero before any rank publishes
+        mc = int(getattr(hb, "multicast_ptr", 0) or 0) if multicast else 0
+        self.multicast = mc != 0
+        self.handle = handle
+        self._rl = rl
+        self._keep = (hb, hf)
+        self.x = handle.exchange_create(self.P, self.rank, k, m, r, [int(p) for p in hb.buffer_ptrs],
+                                        [int(p) for p in hf.buffer_ptrs], mc or None)
+        self.epoch = 0
+
+    def backward(self, bwd, shape, X, W, A, B, dY, dX, dA, dB, accumulate=False, ws=None):
+        """The backward of this rank's token shard with dA, dB summed over all ranks (fp32)."""
+        self.epoch += 1
+        self.handle.backward_exchange(bwd, shape, X, W, A, B, dY, dX, dA, dB, self.x, self.epoch,
+                                      accumulate=accumulate, ws=ws)
+
+    def close(self):
+        if getattr(self, "x", None) is not None:
+            self._rl.exchange_destroy(self.x)
+            self.x = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class _StreamJoin:
     def __init__(self, stream, device):
         self.stream, self.device = stream, device

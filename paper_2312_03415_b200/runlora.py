@@ -75,7 +75,9 @@ EXPORTS = ["runlora_version", "runlora_create", "runlora_destroy", "runlora_flop
            "runlora_workspace_size", "runlora_select", "runlora_forward", "runlora_backward",
            "runlora_backward_params", "runlora_backward_input", "runlora_step_host", "runlora_profile_enable",
            "runlora_profile_read", "runlora_launch_count", "runlora_status_string", "runlora_last_error",
-           "runlora_quantize_w_e4m3", "runlora_workspace_size_wq", "runlora_forward_wq", "runlora_backward_wq"]
+           "runlora_quantize_w_e4m3", "runlora_workspace_size_wq", "runlora_forward_wq", "runlora_backward_wq",
+           "runlora_allreduce_sum_f32", "runlora_exchange_sizes", "runlora_exchange_create", "runlora_exchange_destroy",
+           "runlora_backward_exchange"]
 
 
 def _load():
@@ -108,6 +110,11 @@ def _load():
         "runlora_forward_wq": (I, [P, I, S, P, P, P, P, P, P, P, SZ, P]),
         "runlora_backward_wq": (I, [P, I, S, P, P, P, P, P, P, P, P, P, I, I, P, SZ, P]),
         "runlora_allreduce_sum_f32": (I, [P, C.POINTER(P), I, P, C.c_int64, P]),
+        "runlora_exchange_sizes": (I, [C.c_int64, C.c_int64, C.c_int64, I, C.POINTER(SZ), C.POINTER(SZ)]),
+        "runlora_exchange_create": (I, [P, I, I, C.c_int64, C.c_int64, C.c_int64, C.POINTER(P), C.POINTER(P), P,
+                                        C.POINTER(P)]),
+        "runlora_exchange_destroy": (I, [P]),
+        "runlora_backward_exchange": (I, [P, I, S, P, P, P, P, P, P, P, P, I, I, P, C.c_uint32, P, SZ, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -179,6 +186,18 @@ def workspace_size_wq(shape: Shape) -> int:
     return out.value
 
 
+def exchange_sizes(k, m, r, P):
+    """(buffer bytes, flag bytes) of each rank's fused-exchange buffers (runlora_exchange_sizes)."""
+    b, f = C.c_size_t(), C.c_size_t()
+    _check(_lib.runlora_exchange_sizes(int(k), int(m), int(r), int(P), C.byref(b), C.byref(f)),
+           "runlora_exchange_sizes")
+    return int(b.value), int(f.value)
+
+
+def exchange_destroy(x):
+    _lib.runlora_exchange_destroy(x)
+
+
 def select_by_flops(shape: Shape) -> Plan:
     p = Plan()
     _check(_lib.runlora_select(None, C.byref(shape), BY_FLOPS, None, None, 0, None, C.byref(p)), "runlora_select")
@@ -232,6 +251,26 @@ class Handle:
         arr = (C.c_void_p * len(peer_ptrs))(*[int(p) for p in peer_ptrs])
         _check(_lib.runlora_allreduce_sum_f32(self._h, arr, len(peer_ptrs), _ptr(out), n, _stream(self.device)),
                "runlora_allreduce_sum_f32")
+
+    # ------------------------------------------------- fused DP exchange (NEXT-2)
+    def exchange_create(self, P, rank, k, m, r, buf_ptrs, flag_ptrs, mc_ptr=None):
+        """runlora_exchange_create: this rank's view of the ranks' exchange buffers / flag arrays
+        (device addresses in rank order, as mapped in this process)."""
+        x = C.c_void_p()
+        bufs = (C.c_void_p * P)(*[int(v) for v in buf_ptrs])
+        flags = (C.c_void_p * P)(*[int(v) for v in flag_ptrs])
+        _check(_lib.runlora_exchange_create(self._h, P, rank, k, m, r, bufs, flags, mc_ptr or None, C.byref(x)),
+               "runlora_exchange_create")
+        return x
+
+    def backward_exchange(self, bwd, shape, X, W, A, B, dY, dX, dA, dB, xchg, epoch, accumulate=False, ws=None):
+        """runlora_backward_exchange: the backward with dA, dB summed over the ranks by the dX
+        GEMM launch's idle warps (fp32 gradients)."""
+        ws = self.workspace(shape) if ws is None else ws
+        _check(_lib.runlora_backward_exchange(self._h, int(bwd), C.byref(shape), _ptr(X), _ptr(W), _ptr(A), _ptr(B),
+                                              _ptr(dY), _ptr(dX), _ptr(dA), _ptr(dB), F32, int(bool(accumulate)),
+                                              xchg, int(epoch), _ptr(ws), ws.numel(), _stream(self.device)),
+               "runlora_backward_exchange")
 
     # ------------------------------------------------- quantized frozen W (R18)
     def quantize_w(self, W: torch.Tensor):

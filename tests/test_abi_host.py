@@ -120,3 +120,24 @@ def test_host_step_struct_matches_header(rl):
     assert "#define RUNLORA_ABI_VERSION 2" in src
     assert [f[0] for f in rl.HostStep._fields_][-2:] == ["exchange", "exchange_user"]
     assert C.sizeof(rl.HostStep) == 4 * 4 + 15 * 8 + 2 * 8
+
+
+def test_exchange_sizes_and_null_handle(rl):
+    """Fused exchange geometry (include/runlora.h): two epoch halves of r(k+m) fp32 (rounded up
+    to 64 floats) per rank, one flag per 64-row chunk and rank; argument checks before any
+    device work."""
+    buf, flags = rl.exchange_sizes(4096, 4096, 16, 8)
+    assert buf == 2 * 16 * 8192 * 4 and flags == (8192 // 64) * 8 * 4
+    buf, flags = rl.exchange_sizes(1000, 24, 8, 3)
+    assert buf == 2 * ((1024 * 8 + 63) // 64 * 64) * 4 and flags == 16 * 3 * 4
+    for bad in [(0, 8, 8, 1), (8, 8, 6, 1), (8, 8, 8, 0), (8, 8, 8, 17)]:
+        with pytest.raises(rl.RunLoRAError) as e:
+            rl.exchange_sizes(*bad)
+        assert e.value.status == 1
+    x = C.c_void_p()
+    arr = (C.c_void_p * 1)(4096)
+    assert rl._lib.runlora_exchange_create(None, 1, 0, 8, 8, 8, arr, arr, None, C.byref(x)) == 1
+    s = rl.make_shape(256, 256, 256, 8, rl.BF16)
+    p = C.c_void_p(4096)
+    assert rl._lib.runlora_backward_exchange(None, 1, C.byref(s), p, p, p, p, p, p, p, p, 0, 0, p, 1, p, 1 << 20,
+                                             None) == 1
