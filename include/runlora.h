@@ -209,30 +209,32 @@ runlora_status_t runlora_step_host(runlora_handle_t h, const runlora_shape_t* s,
 /* ---------------------------------------------- quantized frozen weight (QLoRA-style)
  * "functionality to work with quantized model weights to fine-tune models in fashion of
  * QLoRA" (no format given).  Format (R18): FP8 E4M3 (OCP E4M3FN: bias 7,
- * max 448, no infinities) with one fp32 scale per output column:
- *   scale[j] = max_i |W[i, j]| / 448 (1 for an all-zero column),
- *   Wq[i, j] = e4m3_rn_satfinite(W[i, j] / scale[j])      (Wq: k x m bytes, row-major)
- *   W~[i, j] = bf16_rn(fp32(e4m3(Wq[i, j])) * scale[j])   (what the hot path multiplies by).
- * runlora_quantize_w_e4m3: W bf16 [k, m] (device) -> Wq, scale (device; scale 16-byte
- *   aligned, m a multiple of 8).  Asynchronous on `stream`.
+ * max 448, no infinities) with one power-of-two scale per output column:
+ *   e[j]     = clamp(ceil(log2(max_i |W[i, j]| / 448)), -16, 15)   (0 for an all-zero column)
+ *   scale[j] = 2^e[j],  Wq[i, j] = e4m3_rn_satfinite(W[i, j] / scale[j])   (Wq: k x m bytes)
+ *   W~[i, j] = e4m3(Wq[i, j]) · scale[j]   (exact — what the hot path multiplies by)
+ *   diag     = m x 128 bytes, E5M2: row j holds 2^e[j] at column j mod 128, zeros elsewhere
+ *              (the scale as a diagonal matrix the tensor cores multiply Wq by)
+ * runlora_quantize_w_e4m3: W bf16 [k, m] (device) -> Wq, scale, diag (device; 16-byte aligned,
+ *   m a multiple of 16).  Asynchronous on `stream`.
  * runlora_forward_wq / runlora_backward_wq: as runlora_forward / runlora_backward with W
- *   given as (Wq, scale); only Wq + scale persist between calls (half of the bf16 W).  The
- *   dequantization rides in the tensor cores: forward2's W'ᵀ and backward4/5's W' are built
- *   straight from the 1-byte Wq by one GEMM whose FP8 identity tail (I·Wq, exact) lands in a
- *   second accumulator scaled in the epilogue, D = bf16(A·B + W~); forward1 and backward1..3,
- *   which multiply by W~ itself, get it from the same GEMM without the A·B part, written
- *   after the regular workspace.  m must be a multiple of 16 (16-byte row strides of Wq),
- *   else RUNLORA_ERR_ALIGNMENT.  Workspace: runlora_workspace_size_wq bytes. */
+ *   given as (Wq, scale, diag); only those persist between calls (about half of the bf16 W).
+ *   The dequantization rides in the tensor cores: forward2's W'ᵀ and backward4/5's W' are
+ *   built straight from the 1-byte Wq by one GEMM whose FP8 tail multiplies Wq by the scale
+ *   diagonal (kind::f8f6f4, exact) into the same accumulator as A·B, D = bf16(A·B + W~);
+ *   forward1 and backward1..3, which multiply by W~ itself, get it from the same GEMM without
+ *   the A·B part, written after the regular workspace.  m must be a multiple of 16, else
+ *   RUNLORA_ERR_ALIGNMENT.  Workspace: runlora_workspace_size_wq bytes. */
 runlora_status_t runlora_quantize_w_e4m3(runlora_handle_t h, int64_t k, int64_t m, const void* W, void* Wq,
-                                         float* scale, void* stream);
+                                         float* scale, void* diag, void* stream);
 runlora_status_t runlora_workspace_size_wq(const runlora_shape_t* s, int fwd, int bwd, size_t* bytes);
 runlora_status_t runlora_forward_wq(runlora_handle_t h, int fwd, const runlora_shape_t* s, const void* X,
-                                    const void* Wq, const float* scale, const void* A, const void* B, void* Y,
-                                    void* workspace, size_t ws_bytes, void* stream);
+                                    const void* Wq, const float* scale, const void* diag, const void* A,
+                                    const void* B, void* Y, void* workspace, size_t ws_bytes, void* stream);
 runlora_status_t runlora_backward_wq(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X,
-                                     const void* Wq, const float* scale, const void* A, const void* B,
-                                     const void* dY, void* dX, void* dA, void* dB, int grad_dtype, int accumulate,
-                                     void* workspace, size_t ws_bytes, void* stream);
+                                     const void* Wq, const float* scale, const void* diag, const void* A,
+                                     const void* B, const void* dY, void* dX, void* dA, void* dB, int grad_dtype,
+                                     int accumulate, void* workspace, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------- data-parallel exchange (one-shot allreduce)
  * The DP exchange step (token-sharded ranks; a8 reduces the per-rank

@@ -3,11 +3,18 @@ runlora_oracle.py: only tests/ and bench.py's baseline legs may use it).
 
 PAPER.md P:20: "We also provide a functionality to work with quantized model weights to
 fine-tune models in fashion of QLoRA" — no format is given.  The
-format chosen (reading R18) is FP8 E4M3 with one fp32 scale per output column:
+format chosen (reading R18, revised in round 2) is FP8 E4M3 with one power-of-two
+scale per output column (an E8M0-style exponent, as in the OCP MX formats):
 
-    scale[j] = max_i |W[i, j]| / 448   (1 when the column is all zero)
-    Wq[i, j] = e4m3_rne_satfinite(W[i, j] / scale[j])      (fp32 division, then RNE)
-    W~[i, j] = bf16_rne(fp32(e4m3(Wq[i, j]) · scale[j]))   (the bf16 W the hot path uses)
+    e[j]     = clamp(ceil(log2(amax_j / 448)), -16, 15),  amax_j = max_i |W[i, j]|
+               (e[j] = 0 when the column is all zero; amax_j / 448 is an fp32 division)
+    scale[j] = 2^e[j]
+    Wq[i, j] = e4m3_rne_satfinite(W[i, j] / scale[j])      (exact division, then RNE)
+    W~[i, j] = e4m3(Wq[i, j]) · scale[j]                   (exact: 4 significant bits, so
+                                                            also exact in bf16)
+Round 1 used scale = amax/448 (any fp32) and W~ = bf16_rne(e4m3 · scale); the power of two
+makes W~ exact, so the tensor cores can apply the scale as an E5M2 diagonal matrix (the
+clamp is E5M2's range of powers of two, 2^-16 .. 2^15).
 
 E4M3 here is the OCP "E4M3FN" encoding: 1 sign, 4 exponent (bias 7), 3 mantissa bits;
 exponent field 0 = subnormals (m/8 · 2^-6); S.1111.111 = NaN; no infinities; max 448.
@@ -63,16 +70,29 @@ def bf16_rne(x32: np.ndarray) -> np.ndarray:
     return rounded.astype(np.uint32).view(np.float32).astype(np.float64)
 
 
+SCALE_EXP_MIN, SCALE_EXP_MAX = -16, 15
+
+
+def scale_exponent(amax: float) -> int:
+    """e = ceil(log2(fp32(amax / 448))) clamped to [-16, 15]; 0 for amax = 0 (reading R18)."""
+    if amax == 0:
+        return 0
+    x = float(np.float32(np.float32(amax) / np.float32(E4M3_MAX)))
+    m, e = np.frexp(x)                   # x = m · 2^e, 0.5 <= m < 1
+    c = int(e) - 1 if m == 0.5 else int(e)  # ceil(log2 x): exact powers of two stay
+    return min(max(c, SCALE_EXP_MIN), SCALE_EXP_MAX)
+
+
 def quantize_w(W) -> tuple[np.ndarray, np.ndarray]:
-    """(Wq bytes [k, m], scale fp32 [m]) of a bf16-valued W [k, m] (reading R18)."""
+    """(Wq bytes [k, m], scale fp32 [m], powers of two) of a bf16-valued W [k, m] (R18)."""
     W32 = np.asarray(W, dtype=np.float32)
     amax = np.max(np.abs(W32), axis=0)
-    scale = np.where(amax > 0, amax / np.float32(E4M3_MAX), np.float32(1.0)).astype(np.float32)
-    q = e4m3_encode((W32 / scale[None, :]).astype(np.float32))
+    scale = np.array([2.0 ** scale_exponent(a) for a in amax], dtype=np.float32)
+    q = e4m3_encode((W32.astype(np.float64) / scale[None, :].astype(np.float64)).astype(np.float32))
     return q, scale
 
 
 def dequantize_w(Wq, scale) -> np.ndarray:
-    """W~ = bf16(fp32(e4m3(Wq)) · scale) as fp64 values [k, m]."""
-    v = E4M3_TABLE[np.asarray(Wq, dtype=np.uint8)].astype(np.float32)
-    return bf16_rne(v * np.asarray(scale, dtype=np.float32)[None, :])
+    """W~ = e4m3(Wq) · scale as fp64 values [k, m] (exact)."""
+    v = E4M3_TABLE[np.asarray(Wq, dtype=np.uint8)]
+    return v * np.asarray(scale, dtype=np.float64)[None, :]

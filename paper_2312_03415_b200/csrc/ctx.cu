@@ -56,15 +56,6 @@ Ctx::Ctx(int device) : device_(device) {
       identity_ = nullptr;
     }
   }
-  {
-    std::vector<uint8_t> eye8(128 * 128, 0);
-    for (int i = 0; i < 128; ++i) eye8[i * 128 + i] = 0x38;  // E4M3 1.0
-    if (cudaMalloc(&identity8_, eye8.size()) != cudaSuccess ||
-        cudaMemcpy(identity8_, eye8.data(), eye8.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
-      if (identity8_) cudaFree(identity8_);
-      identity8_ = nullptr;
-    }
-  }
   if (prev >= 0) cudaSetDevice(prev);
 }
 
@@ -76,7 +67,6 @@ Ctx::~Ctx() {
   for (auto e : free_events_) cudaEventDestroy(e);
   if (cur_start_) cudaEventDestroy(cur_start_);
   if (identity_) cudaFree(identity_);
-  if (identity8_) cudaFree(identity8_);
   if (trace) cudaFree(trace);
   if (ltrace_) cudaFree(ltrace_);
 }

@@ -106,11 +106,9 @@ struct GemmReq {
   // reductions, summed across ranks by the launch's idle warps (exchange.cuh)
   const void* xdesc;  // device XDesc
   unsigned xepoch;
-  // FP8 identity tail (Prob::tail_fp8): a2 = E4M3 identity, b2 = Wq (uint8), K2 = 128;
-  // out_mode OUT_BF16_WQ with one scale per output row (wq_row_scale) or column
-  bool tail_fp8;
-  const float* wq_scale;
-  bool wq_row_scale;
+  // FP8 tail (ProbX::tail_fp8): 1 = W'ᵀ tile (a2 = scale diagonal E5M2 [m, 128], b2 = Wq,
+  // K2 = 128); 2 = W' / W~ tile (a2 = Wq, b2 = scale diagonal, K2 = BN); BN = 256, TMA store
+  int tail_fp8;
 };
 
 
@@ -125,8 +123,7 @@ class Ctx {
   bool pdl() const { return pdl_; }    // programmatic dependent launch (env RUNLORA_PDL=0 disables)
   // 128x128 bf16 identity (device): A operand of the block-diagonal tail that adds W in W + A·B
   const void* identity() const { return identity_; }
-  // 128x128 E4M3 identity (1.0 = 0x38): A operand of the FP8 tail that dequantises Wq (R18)
-  const void* identity8() const { return identity8_; }
+
   // debug timeline buffer (env RUNLORA_TRACE=<kernel id>): see GemmArgs::trace
   unsigned long long* trace = nullptr;
   unsigned long long* ltrace_ = nullptr;
@@ -182,7 +179,6 @@ class Ctx {
   int num_sms_ = 148;
   int main_cg_ = 2;
   void* identity_ = nullptr;
-  void* identity8_ = nullptr;
   bool tma_store_main_ = false;   // env RUNLORA_TMA_STORE_MAIN=1
   bool main_wide_ = true;
   double wide_cost_a_ = 1.66, wide_cost_e_ = 443.0;
@@ -237,7 +233,8 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
 cudaError_t launch_splitk_reduce(Ctx& ctx, const ReduceJob* jobs, int njobs, cudaStream_t s);
 // Quantized frozen weight (quant.cu): W[k, m] bf16 -> Wq e4m3 bytes + scale[m] fp32, and back
 // to bf16 (m multiple of 8, scale 16-byte aligned).
-cudaError_t launch_quantize_w(Ctx& ctx, const void* W, int64_t k, int64_t m, void* Wq, float* scale, cudaStream_t s);
+cudaError_t launch_quantize_w(Ctx& ctx, const void* W, int64_t k, int64_t m, void* Wq, float* scale, void* diag,
+                              cudaStream_t s);
 constexpr int kMaxPeers = 16;  // runlora_allreduce_sum_f32
 struct XDesc;
 struct XSlabs;

@@ -97,9 +97,7 @@ cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, GemmArgs& g, cudaStream_t s) {
 cudaError_t dispatch_tc(Ctx& ctx, int bn_max, int cg, bool occ2, bool tma_store, const Tmaps& tm, GemmArgs& g,
                         cudaStream_t s) {
   if (tma_store) {
-    // (the quantized-W builds run 128-wide units on this 256-wide kernel: two accumulators of
-    // 128 columns per TMEM slot, Prob::tail_fp8)
-    if (cg == 1 && bn_max <= 256) return run_tc<256, 1, 1, 3>(ctx, tm, g, s);
+    if (cg == 1 && bn_max == 256) return run_tc<256, 1, 1, 3>(ctx, tm, g, s);
     if (cg == 2 && bn_max == 256) return run_tc<256, 2, 1, 3>(ctx, tm, g, s);
     if (cg == 2 && bn_max == 512) return run_tc<512, 2, 1, 3>(ctx, tm, g, s);
     return cudaErrorNotSupported;
@@ -280,8 +278,7 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
       if (err) *err = "tc_gemm: 512-wide tiles need a CTA pair, K-major B and a plain output";
       return cudaErrorInvalidValue;
     }
-    if (r.tma_store && (!(r.out_mode == OUT_BF16 || (r.out_mode == OUT_BF16_WQ && r.tail_fp8)) ||
-                        (r.BN < 256 && !r.tail_fp8) || r.splits > 1)) {
+    if (r.tma_store && (r.out_mode != OUT_BF16 || r.BN < 256 || r.splits > 1)) {
       if (err) *err = "tc_gemm: TMA-store epilogue needs a plain bf16 output with 256- or 512-wide tiles";
       return cudaErrorInvalidValue;
     }
@@ -303,13 +300,14 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
     if (!ctx.tmap(r.a, a_box, &tm.m[q][0], err, 128, a3 ? 2 : 0) ||
         !ctx.tmap(r.b, b_box, &tm.m[q][1], err, b_swz, b3 ? nb / b_cw : 0))
       return cudaErrorInvalidValue;
-    if (r.tail_fp8) {  // E4M3 identity and Wq: boxes of 128 rows x 128 bytes
-      if (r.K2 != 128 || cg != 1 || r.BN > 128 || r.out_mode != OUT_BF16_WQ || !r.tma_store || !r.wq_scale ||
-          !ctx.tmap(r.a2, 128, &tm.m[q][2], err, 128, 0, 1) || !ctx.tmap(r.b2, 128, &tm.m[q][3], err, 128, 0, 1)) {
-        if (err && err->empty()) *err = "tc_gemm: the FP8 tail needs K2 = 128, BN <= 128, one CTA, the WQ epilogue";
+    if (r.tail_fp8) {  // Wq (E4M3) and the scale diagonal (E5M2), 128-byte K rows
+      const bool ok = (r.tail_fp8 == 1 || r.tail_fp8 == 2) && cg == 1 && r.BN == 256 && r.tma_store &&
+                      r.K2 == (r.tail_fp8 == 1 ? 128 : r.BN) && !r.tail_diag;
+      if (!ok || !ctx.tmap(r.a2, 128, &tm.m[q][2], err, 128, 0, 1) ||
+          !ctx.tmap(r.b2, r.tail_fp8 == 1 ? r.BN : 128, &tm.m[q][3], err, 128, 0, 1)) {
+        if (err && err->empty()) *err = "tc_gemm: the FP8 tail needs 256-wide single-CTA tiles and the TMA store";
         return cudaErrorInvalidValue;
-      }
-    } else if (r.K2 > 0) {
+      }    } else if (r.K2 > 0) {
       if (!ctx.tmap(r.a2, a_box, &tm.m[q][2], err, 128, a3 ? 2 : 0) ||
           !ctx.tmap(r.b2, b_box, &tm.m[q][3], err, b_swz, b3 ? nb / b_cw : 0))
         return cudaErrorInvalidValue;
@@ -359,12 +357,10 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
       return cudaErrorInvalidValue;
     }
     p.tail_diag = r.tail_diag ? 1 : 0;
-    if (r.tail_fp8) {
-      px.tail_fp8 = 1;
-      p.nk2 = 1;
-      px.idesc2 = idesc_e4m3(kBM, r.BN, r.a_mn, r.b_mn);
-      px.wq_scale = r.wq_scale;
-      px.wq_row_scale = r.wq_row_scale ? 1 : 0;
+    if (r.tail_fp8) {  // mode 1: A2 = diagonal (E5M2), B2 = Wq; mode 2: A2 = Wq, B2 = diagonal
+      px.tail_fp8 = r.tail_fp8;
+      p.nk2 = r.tail_fp8 == 1 ? 1 : r.BN / 128;
+      px.idesc2 = r.tail_fp8 == 1 ? idesc_f8(kBM, r.BN, kE5M2, kE4M3) : idesc_f8(kBM, 128, kE4M3, kE5M2);
     }
     if (r.fixup) {
       if (!(r.out_mode == OUT_F32 || r.out_mode == OUT_F32_FOLD) || cg != 1 || !r.counters || !r.fx_out ||

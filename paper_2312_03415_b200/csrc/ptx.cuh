@@ -324,12 +324,13 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
          | ((uint32_t)(M >> 4) << 24);   // M >> 4
 }
 
-// Instruction descriptor for kind::f8f6f4 with E4M3 A and B: D fp32, majors, N, M
-// (a_format = b_format = 0 = E4M3).
-__host__ __device__ constexpr uint32_t idesc_e4m3(int M, int N, bool a_mn, bool b_mn) {
+// Instruction descriptor for kind::f8f6f4, both operands K-major: D fp32, A / B formats
+// (E4M3 = 0, E5M2 = 1), N, M.
+constexpr uint32_t kE4M3 = 0, kE5M2 = 1;
+__host__ __device__ constexpr uint32_t idesc_f8(int M, int N, uint32_t a_fmt, uint32_t b_fmt) {
   return (1u << 4)                       // c_format = F32
-         | ((a_mn ? 1u : 0u) << 15)      // a_major
-         | ((b_mn ? 1u : 0u) << 16)      // b_major
+         | (a_fmt << 7)                  // a_format
+         | (b_fmt << 10)                 // b_format
          | ((uint32_t)(N >> 3) << 17)    // N >> 3
          | ((uint32_t)(M >> 4) << 24);   // M >> 4
 }

@@ -1,12 +1,14 @@
 // Quantized frozen weight (QLoRA-style; format:
-// DESIGN.md reading R18): W ≈ scale[j] · e4m3(Wq[i, j]) with one fp32 scale per output
-// column.  Three HBM-bound kernels:
-//   colmax      scale[j] <- bits of max_i |W[i, j]|           (atomicMax on non-negative floats)
-//   quantize    Wq[i, j] = e4m3_rn_satfinite(W[i, j] / s[j]),  s[j] = amax > 0 ? amax/448 : 1
-//   finalize    scale[j] <- s[j]
-// The way back, W~[i, j] = bf16_rn(fp32(e4m3(Wq[i, j])) · scale[j]), is not a kernel of its own:
-// the tcgen05 GEMM's FP8 identity tail does it inside the W' / W'ᵀ / W~ builds (runlora.cu
-// wprime_q, tc_gemm.cuh Prob::tail_fp8).
+// DESIGN.md reading R18): W ≈ 2^e[j] · e4m3(Wq[i, j]) with one power-of-two scale per output
+// column.  Four HBM-bound kernels:
+//   colmax      amax[j] <- bits of max_i |W[i, j]|          (atomicMax on non-negative floats)
+//   quantize    Wq[i, j] = e4m3_rn_satfinite(W[i, j] / 2^e[j]),
+//               e[j] = clamp(ceil(log2(amax_j / 448)), -16, 15) (0 for an all-zero column)
+//   finalize    scale[j] <- 2^e[j]
+//   diagonal    D[j, c] = (c == j mod 128) ? e5m2(2^e[j]) : 0     (m x 128 bytes)
+// The way back, W~ = e4m3(Wq) · 2^e (exact), is not a kernel of its own: the tcgen05 GEMM
+// multiplies Wq by the E5M2 diagonal D in its FP8 tail (runlora.cu wprime_q, tc_gemm.cuh
+// Prob::tail_fp8), inside the W' / W'ᵀ / W~ builds.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
@@ -17,7 +19,15 @@
 namespace runlora {
 namespace {
 
-__device__ __forceinline__ float col_scale(float amax) { return amax > 0.f ? __fdiv_rn(amax, 448.f) : 1.f; }
+// e = clamp(ceil(log2(fp32(amax / 448))), -16, 15), 0 for amax = 0 (oracle/quant.py scale_exponent)
+__device__ __forceinline__ int scale_exp(float amax) {
+  if (!(amax > 0.f)) return 0;
+  int e;
+  const float m = frexpf(__fdiv_rn(amax, 448.f), &e);  // x = m · 2^e, m in [0.5, 1)
+  const int c = m == 0.5f ? e - 1 : e;
+  return c < -16 ? -16 : c > 15 ? 15 : c;
+}
+__device__ __forceinline__ float col_scale(float amax) { return __int_as_float((scale_exp(amax) + 127) << 23); }
 
 // grid (ceil(m/256), row_splits): thread = one column, a strided share of the rows
 __global__ void __launch_bounds__(256) colmax_kernel(const __nv_bfloat16* __restrict__ W, int64_t k, int64_t m,
@@ -58,6 +68,27 @@ __global__ void __launch_bounds__(256) finalize_scale_kernel(float* __restrict__
   if (j < m) scale[j] = col_scale(scale[j]);  // amax bits (as float) -> scale
 }
 
+// m rows of 128 bytes; thread = 16 bytes of a row: zeros except the E5M2 code of 2^e[j] at
+// column j mod 128 (e5m2: bias 15, 2 mantissa bits; 2^-15 and 2^-16 are subnormals)
+__global__ void __launch_bounds__(256) diag_kernel(const float* __restrict__ scale, int64_t m, uint4* __restrict__ D) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int64_t total = m * 8;
+  for (int64_t t = blockIdx.x * 256ll + threadIdx.x; t < total; t += (int64_t)gridDim.x * 256) {
+    const int64_t j = t >> 3;
+    const int c0 = (int)(t & 7) * 16, cj = (int)(j & 127);
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (cj >= c0 && cj < c0 + 16) {
+      const int e = (int)((__float_as_uint(scale[j]) >> 23) & 0xFF) - 127;
+      const uint32_t code = e >= -14 ? (uint32_t)(e + 15) << 2 : e == -15 ? 0x02u : 0x01u;
+      uint32_t w[4] = {0u, 0u, 0u, 0u};
+      w[(cj - c0) >> 2] = code << (8 * ((cj - c0) & 3));
+      v = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    D[t] = v;
+  }
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch(Ctx& ctx, KernelId kid, void (*kern)(KArgs...), dim3 grid, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -83,7 +114,8 @@ unsigned elem_blocks(Ctx& ctx, int64_t total_threads) {
 
 }  // namespace
 
-cudaError_t launch_quantize_w(Ctx& ctx, const void* W, int64_t k, int64_t m, void* Wq, float* scale, cudaStream_t s) {
+cudaError_t launch_quantize_w(Ctx& ctx, const void* W, int64_t k, int64_t m, void* Wq, float* scale, void* diag,
+                              cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(scale, 0, sizeof(float) * m, s);
   if (e != cudaSuccess) return e;
   const unsigned cols = (unsigned)((m + 255) / 256);
@@ -95,7 +127,10 @@ cudaError_t launch_quantize_w(Ctx& ctx, const void* W, int64_t k, int64_t m, voi
              static_cast<const __nv_bfloat16*>(W), k, m, reinterpret_cast<const unsigned*>(scale),
              static_cast<uint8_t*>(Wq));
   if (e != cudaSuccess) return e;
-  return launch(ctx, KID_QUANT, finalize_scale_kernel, dim3(cols), s, scale, m);
+  e = launch(ctx, KID_QUANT, finalize_scale_kernel, dim3(cols), s, scale, m);
+  if (e != cudaSuccess) return e;
+  return launch(ctx, KID_QUANT, diag_kernel, dim3(elem_blocks(ctx, m * 8)), s, static_cast<const float*>(scale), m,
+                static_cast<uint4*>(diag));
 }
 
 }  // namespace runlora

@@ -550,17 +550,19 @@ runlora_status_t wprime_t_bf16(Ctx& c, const runlora_shape_t& s, const void* W, 
 }
 
 // ------------------------------------------------------------ quantized W (R18)
-// Wq [k, m] E4M3 bytes with one fp32 scale per column: W~ = bf16(fp32(e4m3(Wq))·scale).
+// Wq [k, m] E4M3 bytes with one power-of-two scale 2^e[j] per column; D [m, 128] E5M2 bytes:
+// row j holds 2^e[j] at column j mod 128 (the scale diagonal, built by the quantizer).
 struct QW {
   const void* q;
   const float* scale;
+  const void* diag;
 };
 
 // W' = W~ + A·B (transposed = false: [k, m], the dX operand of backward4/5), W'ᵀ (transposed:
 // [m, k], forward2's B operand), or W~ alone (ab = false: the x1 variants' W) straight from
-// the 1-byte Wq: ONE GEMM whose fp8 identity tail I·Wq (kind::f8f6f4, exact) lands in a second
-// accumulator that the epilogue scales — D = bf16(A·B + bf16(I·Wq · scale)), the rounding of
-// R18 — so W is read as 1 byte per element and no bf16 copy of W~ is written first.
+// the 1-byte Wq: ONE GEMM whose FP8 tail multiplies Wq by the E5M2 scale diagonal (kind::
+// f8f6f4) into the same fp32 accumulator as A·B — W~ = e4m3 · 2^e is exact — so the epilogue
+// is the plain bf16 TMA store: D = bf16(fp32(A·B) + W~), W read as 1 byte per element.
 runlora_status_t wprime_q(Ctx& c, const runlora_shape_t& s, const QW& w, const void* A, const void* B, void* D,
                           bool transposed, bool ab, cudaStream_t st) {
   GemmReq q = base_req((int)(transposed ? s.m : s.k), (int)(transposed ? s.k : s.m),
@@ -570,28 +572,26 @@ runlora_status_t wprime_q(Ctx& c, const runlora_shape_t& s, const QW& w, const v
     q.b = mat(c.identity(), 128, 128);
     q.b_mn = true;
     q.K1 = 0;
-  } else if (transposed) {  // D[j, i] = Σ_r B[r, j]·A[i, r] + s[j]·Wq[i, j]
+  } else if (transposed) {  // D[j, i] = Σ_r B[r, j]·A[i, r] + Σ_j' diag[j, j']·Wq[i, j']
     q.a = mat(B, s.r, s.m);
     q.a_mn = true;
     q.b = mat(A, s.k, s.r);
     q.K1 = (int)s.r;
-  } else {  // D[i, j] = Σ_r A[i, r]·B[r, j] + s[j]·Wq[i, j]
+  } else {  // D[i, j] = Σ_r A[i, r]·B[r, j] + Σ_j' Wq[i, j']·diag[j', j]
     q.a = mat(A, s.k, s.r);
     q.b = mat(B, s.r, s.m);
     q.b_mn = true;
     q.K1 = (int)s.r;
   }
-  q.a2 = mat(c.identity8(), 128, 128);
-  q.b2 = mat(w.q, s.k, s.m);  // bytes: K-major for W'ᵀ (K = j'), MN-major for W' / W~ (K = i')
-  q.K2 = 128;
-  q.tail_diag = true;
-  q.tail_fp8 = true;
-  q.wq_scale = w.scale;
-  q.wq_row_scale = transposed;
-  q.out_mode = OUT_BF16_WQ;
+  const DeviceMat wq{w.q, s.k, s.m, s.m}, dg{w.diag, s.m, 128, 128};  // bytes
+  q.BN = 256;
+  q.tail_fp8 = transposed ? 1 : 2;
+  q.a2 = transposed ? dg : wq;
+  q.b2 = transposed ? wq : dg;
+  q.K2 = transposed ? 128 : q.BN;
+  q.out_mode = OUT_BF16;
   q.D = D;
   q.ldd = transposed ? s.k : s.m;
-  q.BN = 128;  // two accumulators (A·B and I·Wq) of 128 columns per TMEM slot
   q.tma_store = true;
   return gemm(c, q, st);
 }
@@ -1370,16 +1370,17 @@ runlora_status_t runlora_backward_input(runlora_handle_t h, int bwd, const runlo
 
 // ------------------------------------------------ quantized frozen weight (R18)
 runlora_status_t runlora_quantize_w_e4m3(runlora_handle_t h, int64_t k, int64_t m, const void* W, void* Wq,
-                                         float* scale, void* stream) {
+                                         float* scale, void* diag, void* stream) {
   RL_TRY(check_handle(h));
   if (k <= 0 || m <= 0) return fail(RUNLORA_ERR_INVALID_ARG, "k and m must be >= 1");
-  if (m & 7) return fail(RUNLORA_ERR_ALIGNMENT, "m must be a multiple of 8");
+  if (m & 15) return fail(RUNLORA_ERR_ALIGNMENT, "m must be a multiple of 16 (16-byte rows of Wq)");
   RL_TRY(check_ptr(W, "W"));
   RL_TRY(check_ptr(Wq, "Wq"));
   RL_TRY(check_ptr(scale, "scale"));
+  RL_TRY(check_ptr(diag, "diag"));
   CallLock lk(h->ctx->call_mu);
   DeviceGuard dg(h->ctx->device());
-  cudaError_t e = launch_quantize_w(*h->ctx, W, k, m, Wq, scale, static_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_quantize_w(*h->ctx, W, k, m, Wq, scale, diag, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "quantize launch");
   return RUNLORA_OK;
 }
@@ -1413,8 +1414,8 @@ runlora_status_t runlora_workspace_size_wq(const runlora_shape_t* s, int fwd, in
 
 namespace {
 // Validates the quantized-W arguments; binds the regular workspace and the W~ region after it.
-runlora_status_t bind_wq(runlora_handle_t h, const runlora_shape_t* s, const void* Wq, const float* scale, void* ws,
-                         size_t ws_bytes, Bufs* b, void** wdq) {
+runlora_status_t bind_wq(runlora_handle_t h, const runlora_shape_t* s, const void* Wq, const float* scale,
+                         const void* diag, void* ws, size_t ws_bytes, Bufs* b, void** wdq) {
   RL_TRY(check_handle(h));
   RL_TRY(check_shape(s));
   if (s->dtype != RUNLORA_BF16) return fail(RUNLORA_ERR_DTYPE, "quantized W needs bf16 operands");
@@ -1422,6 +1423,7 @@ runlora_status_t bind_wq(runlora_handle_t h, const runlora_shape_t* s, const voi
     return fail(RUNLORA_ERR_ALIGNMENT, "quantized W needs m a multiple of 16 (16-byte TMA row strides of the 1-byte Wq)");
   RL_TRY(check_ptr(Wq, "Wq"));
   RL_TRY(check_ptr(scale, "scale"));
+  RL_TRY(check_ptr(diag, "diag"));
   if (!ws) return fail(RUNLORA_ERR_INVALID_ARG, "workspace is NULL");
   const size_t main = layout_of(*s).total;
   if (ws_bytes < main + al((size_t)s->k * s->m * 2)) {
@@ -1439,16 +1441,16 @@ runlora_status_t bind_wq(runlora_handle_t h, const runlora_shape_t* s, const voi
 // forward2 builds W'ᵀ straight from Wq (one fused launch); forward1 needs W~ itself as its
 // main B operand: the same converter writes it into the workspace tail first.
 runlora_status_t runlora_forward_wq(runlora_handle_t h, int fwd, const runlora_shape_t* s, const void* X,
-                                    const void* Wq, const float* scale, const void* A, const void* B, void* Y,
-                                    void* ws, size_t ws_bytes, void* stream) {
+                                    const void* Wq, const float* scale, const void* diag, const void* A,
+                                    const void* B, void* Y, void* ws, size_t ws_bytes, void* stream) {
   Bufs b;
   void* wdq = nullptr;
-  RL_TRY(bind_wq(h, s, Wq, scale, ws, ws_bytes, &b, &wdq));
+  RL_TRY(bind_wq(h, s, Wq, scale, diag, ws, ws_bytes, &b, &wdq));
   RL_TRY(validate_forward(h, fwd, s, X, wdq, A, B, Y));
   CallLock lk(h->ctx->call_mu);
   DeviceGuard dg(h->ctx->device());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const QW qw{Wq, scale};
+  const QW qw{Wq, scale, diag};
   if (fwd == 1) RL_TRY(wprime_q(*h->ctx, *s, qw, nullptr, nullptr, wdq, false, false, st));
   RL_TRY(forward_bf16(*h->ctx, fwd, *s, X, wdq, A, B, Y, b, st, fwd == 2 ? &qw : nullptr));
   return post_launch();
@@ -1457,18 +1459,18 @@ runlora_status_t runlora_forward_wq(runlora_handle_t h, int fwd, const runlora_s
 // backward4/5 build W' straight from Wq for dX; backward1..3 multiply dX by W~ itself
 // (converter into the workspace tail); the adapter gradients never touch W.
 runlora_status_t runlora_backward_wq(runlora_handle_t h, int bwd, const runlora_shape_t* s, const void* X,
-                                     const void* Wq, const float* scale, const void* A, const void* B,
-                                     const void* dY, void* dX, void* dA, void* dB, int grad_dtype, int accumulate,
-                                     void* ws, size_t ws_bytes, void* stream) {
+                                     const void* Wq, const float* scale, const void* diag, const void* A,
+                                     const void* B, const void* dY, void* dX, void* dA, void* dB, int grad_dtype,
+                                     int accumulate, void* ws, size_t ws_bytes, void* stream) {
   Bufs b;
   void* wdq = nullptr;
-  RL_TRY(bind_wq(h, s, Wq, scale, ws, ws_bytes, &b, &wdq));
+  RL_TRY(bind_wq(h, s, Wq, scale, diag, ws, ws_bytes, &b, &wdq));
   RL_TRY(validate_params(h, bwd, s, X, A, B, dY, dA, dB, grad_dtype));
   if (dX) RL_TRY(validate_input(h, bwd, s, wdq, A, B, dY, dX));
   CallLock lk(h->ctx->call_mu);
   DeviceGuard dg(h->ctx->device());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const QW qw{Wq, scale};
+  const QW qw{Wq, scale, diag};
   std::vector<ReduceJob> side;
   RL_TRY(params_bf16(*h->ctx, bwd, *s, X, A, B, dY, dA, dB, grad_dtype == RUNLORA_BF16, accumulate != 0, b, st,
                      dX ? &side : nullptr));

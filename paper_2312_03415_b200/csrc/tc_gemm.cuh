@@ -40,15 +40,12 @@
 
 namespace runlora {
 
-enum OutMode : int { OUT_BF16 = 0, OUT_BF16_ADD = 1, OUT_F32 = 2, OUT_F32_FOLD = 4, OUT_BF16_WQ = 5 };
+enum OutMode : int { OUT_BF16 = 0, OUT_BF16_ADD = 1, OUT_F32 = 2, OUT_F32_FOLD = 4 };
 // OUT_BF16 with splits: split s of the K reduction writes its own bf16 partial at
 //                 D + s * split_stride (e.g. side-by-side column blocks of a partial matrix).
 // OUT_F32_FOLD:   the accumulator's bn = fold * fold_w columns are fold column blocks whose sum
 //                 (fixed block order, fp32) is the output: fp32 slab D[split][M][ldd], fold_w cols.
 // OUT_BF16_ADD:   D[i, j] = acc[i, j] + Cin[i * ldc + j]
-// OUT_BF16_WQ:    (with tail_fp8) D = bf16(acc + bf16(acc_q · scale)), acc_q the fp8 tail's own
-//                 accumulator (TMEM columns [bn, 2 bn) of the slot), scale per output row or
-//                 column (wq_row_scale); acc = 0 when the problem has no main K (nk1 = 0).
 
 struct Prob {
   int M, N;              // output extent (epilogue masks rows >= M, cols >= N)
@@ -89,15 +86,15 @@ struct ProbX {
   //   out[i, c] (or out[c, i] when fx_transpose) {=, +=} sum_s slab[s][i][c],  c < fx_cols,
   // as fp32 or bf16.  counters: one int per output tile, zero before the launch (the
   // launch that zeroes them is GemmArgs::zero_ptr of an earlier launch in the stream).
-  // FP8 identity tail (quantized W, R18): ONE tail k-block of 128 E4M3 K-elements
-  // (one 128-byte swizzle row) — A2 the 128x128 E4M3 identity, B2 the Wq rows of this tile —
-  // issued as kind::f8f6f4 MMAs (idesc2) into a second accumulator at slot column bn, so that
-  // the epilogue can scale it (OUT_BF16_WQ): the dequantisation rides in the tensor cores and
-  // W is read as 1 byte per element.
+  // FP8 tail (quantized W, R18): W~ = e4m3(Wq) · 2^e[col] enters the SAME fp32
+  // accumulator as A·B through kind::f8f6f4 MMAs (idesc2) against the E5M2 diagonal D of the
+  // power-of-two column scales — exact, so the epilogue is the plain bf16 store and W is read
+  // as 1 byte per element.  1: W'ᵀ tile (rows j): one tail block, A2 = D rows of this tile,
+  // B2 = Wq rows of the tile's columns at K = j' (MMA N = bn).  2: W' / W~ tile (rows i): one
+  // tail block per 128 columns h, A2 = Wq rows of this tile at K = n0 + 128 h, B2 = D rows
+  // n0 + 128 h (MMA N = 128 into accumulator columns [128 h, +128)).  Both K-major.
   int tail_fp8;
   uint32_t idesc2;
-  const float* wq_scale;
-  int wq_row_scale;
   int fixup;
   int* counters;
   void* fx_out;
@@ -552,7 +549,9 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
           // a ragged 512-wide tile loads one B box per CTA
           const uint32_t full_tx = (BN_MAX > SLOT_W && p.bn > SLOT_W && nh == 1) ? p.stage_tx - CG * kBHalf : p.stage_tx;
           const uint32_t tx = g.dbg == 5 ? (uint32_t)(CG * kBM * kBK * 2)
-                              : skip_a ? full_tx - (uint32_t)(CG * kBM * kBK * 2) : full_tx;
+                              : skip_a ? full_tx - (uint32_t)(CG * kBM * kBK * 2)
+                              : (fp8_tail && px.tail_fp8 == 2 && i0 >= nmain) ? 2u * 128u * 128u  // two 16 KB boxes
+                                                                             : full_tx;
           if (leader) mbar_arrive_expect_tx(fb, tx * (uint32_t)natoms);
           for (int at = 0; at < natoms; ++at) {
             const int i = i0 + at;
@@ -571,12 +570,15 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
             const int kc = (tail ? (i - nmain) : (kb0 + ki)) * kBK;
             const int ma = diag ? 0 : m0;          // identity tail: rows of I
             const int kcb = diag ? m0 + kc : kc;   // identity tail: B2 rows of this tile
-            if (fp8_tail && tail) {
-              // the 128x128 E4M3 identity and this tile's 128 Wq rows (one 128-byte K row each):
-              // K-major B2 is Wq[n0.., m0..] (x = K = m0), MN-major B2 is Wq[m0.., n0..] (x = N)
-              tma_load_2d<CG>(ta, fb, a, 0, 0, p.hint_a);
-              if (!p.b_mn) tma_load_2d<CG>(tb, fb, b, m0, n0, p.hint_b);
-              else tma_load_2d<CG>(tb, fb, b, n0, m0, p.hint_b);
+            if (fp8_tail && tail) {  // ProbX::tail_fp8 (expect_tx set below for mode 2)
+              const int h = i - nmain;
+              if (px.tail_fp8 == 1) {  // D rows m0.. (E5M2); Wq rows n0.. at K = m0 (E4M3)
+                tma_load_2d<CG>(ta, fb, a, 0, m0, p.hint_a);
+                tma_load_2d<CG>(tb, fb, b, m0, n0, p.hint_b);
+              } else {                 // Wq rows m0.. at K = n0 + 128 h (E4M3); D rows n0 + 128 h (E5M2)
+                tma_load_2d<CG>(ta, fb, a, n0 + 128 * h, m0, p.hint_a);
+                tma_load_2d<CG>(tb, fb, b, 0, n0 + 128 * h, p.hint_b);
+              }
               continue;
             }
             if (skip_a) {
@@ -657,14 +659,14 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
           const uint32_t a_addr = smem_u32(sA + st * C::A_BYTES + at * C::A_ATOM);
           const uint32_t b_addr = smem_u32(sB + st * C::B_BYTES + at * C::B_ATOM);
           if (fp8_tail && i >= nmain) {
-            // 4 K-steps of 32 E4M3 elements (32 B along a K-major row, 32 rows = 4 KB of an
-            // MN-major tile) into the second accumulator at column bn; the first step starts it
-            const uint64_t a8 = smem_desc(0, p.a_mn ? 16384u : 16u, 1024u, 2u);
-            const uint64_t b8 = smem_desc(0, p.b_mn ? 16384u : 16u, 1024u, 2u);
-            const uint32_t as = p.a_mn ? 4096u : 32u, bs = p.b_mn ? 4096u : 32u;
+            // 4 K-steps of 32 FP8 elements (32 B along the 128-byte K rows) into the main
+            // accumulator (mode 2: columns [128 h, +128)); starts it when there is no main K
+            const uint64_t d8 = smem_desc(0, 16u, 1024u, 2u);
+            const uint32_t dcol = px.tail_fp8 == 2 ? (uint32_t)(128 * (i - nmain)) : 0u;
             for (int j = 0; j < 4; ++j)
-              umma_f8(d_tmem + (uint32_t)p.bn, a8 | (uint64_t)(((a_addr + j * as) >> 4) & 0x3FFF),
-                      b8 | (uint64_t)(((b_addr + j * bs) >> 4) & 0x3FFF), px.idesc2, j > 0 ? 1u : 0u);
+              umma_f8(d_tmem + dcol, d8 | (uint64_t)(((a_addr + 32 * j) >> 4) & 0x3FFF),
+                      d8 | (uint64_t)(((b_addr + 32 * j) >> 4) & 0x3FFF), px.idesc2,
+                      (nmain > 0 || j > 0) ? 1u : 0u);
             continue;
           }
           for (int j = 0; j < (g.dbg == 2 ? 0 : ksteps); ++j) {
@@ -843,52 +845,6 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
           uint8_t* stg = smem + STAGES * C::STAGE_BYTES + q * (C::STG_BUFS * 4096);
           const int nch = min(bw, p.N - nc + 63) / 64;  // 64-column chunks inside N
           const CUtensorMap* dmap = &tm.m[t.prob][4];
-          if (kFp8Tail && p.out_mode == OUT_BF16_WQ) {
-            // D = bf16(acc + bf16(acc_q · scale)); acc_q at slot column bn (Prob::tail_fp8)
-            const float srow = (px.wq_row_scale && row < p.M) ? __ldg(px.wq_scale + row) : 0.f;
-#pragma unroll 1
-            for (int i = 0; i < nch; ++i) {
-              uint32_t pk[32];
-#pragma unroll
-              for (int hh = 0; hh < 2; ++hh) {
-                uint32_t va[32], vq[32];
-                const int cc = 64 * i + 32 * hh;  // tile column of this half chunk
-                tmem_ld_32x32b_x32(t_row + (uint32_t)(p.bn + cc), vq);
-                if (p.nk1 > 0) tmem_ld_32x32b_x32(t_row + (uint32_t)cc, va);
-                tmem_ld_wait();
-                reg_fence32(vq);
-                if (p.nk1 > 0) reg_fence32(va);
-                float sc[32];
-                if (px.wq_row_scale) {
-#pragma unroll
-                  for (int x = 0; x < 32; ++x) sc[x] = srow;
-                } else {
-#pragma unroll
-                  for (int x = 0; x < 32; x += 4) {
-                    const int col = nc + cc + x;
-                    const float4 s4 = col < p.N ? __ldg(reinterpret_cast<const float4*>(px.wq_scale + col))
-                                                : make_float4(0.f, 0.f, 0.f, 0.f);
-                    sc[x] = s4.x, sc[x + 1] = s4.y, sc[x + 2] = s4.z, sc[x + 3] = s4.w;
-                  }
-                }
-#pragma unroll
-                for (int x = 0; x < 32; x += 2) {
-                  // W~ = bf16(e4m3 · scale) (R18) for a pair in ONE packed conversion (the single
-                  // float->bf16 conversion runs on the quarter-rate XU pipe), then + the fp32 A·B
-                  // and one rounding
-                  const uint32_t w2 = pack_bf16x2(__uint_as_float(vq[x]) * sc[x], __uint_as_float(vq[x + 1]) * sc[x + 1]);
-                  if (p.nk1 > 0) {
-                    const float w0 = __uint_as_float(w2 << 16) + __uint_as_float(va[x]);
-                    const float w1 = __uint_as_float(w2 & 0xFFFF0000u) + __uint_as_float(va[x + 1]);
-                    pk[16 * hh + x / 2] = pack_bf16x2(w0, w1);
-                  } else {
-                    pk[16 * hh + x / 2] = w2;
-                  }
-                }
-              }
-              stage_store_packed<C::STG_BUFS>(pk, stg, st_it, lane, dmap, nc + 64 * i, m0 + q * 32);
-            }
-          } else
 #pragma unroll 1
           for (int i = 0; i < nch; ++i) {
             uint32_t v[2][32];

@@ -105,10 +105,10 @@ def _load():
         "runlora_launch_count": (U64, [P]),
         "runlora_status_string": (C.c_char_p, [I]),
         "runlora_last_error": (C.c_char_p, []),
-        "runlora_quantize_w_e4m3": (I, [P, C.c_int64, C.c_int64, P, P, P, P]),
+        "runlora_quantize_w_e4m3": (I, [P, C.c_int64, C.c_int64, P, P, P, P, P]),
         "runlora_workspace_size_wq": (I, [S, I, I, C.POINTER(SZ)]),
-        "runlora_forward_wq": (I, [P, I, S, P, P, P, P, P, P, P, SZ, P]),
-        "runlora_backward_wq": (I, [P, I, S, P, P, P, P, P, P, P, P, P, I, I, P, SZ, P]),
+        "runlora_forward_wq": (I, [P, I, S, P, P, P, P, P, P, P, P, SZ, P]),
+        "runlora_backward_wq": (I, [P, I, S, P, P, P, P, P, P, P, P, P, P, I, I, P, SZ, P]),
         "runlora_allreduce_sum_f32": (I, [P, C.POINTER(P), I, P, C.c_int64, P]),
         "runlora_exchange_sizes": (I, [C.c_int64, C.c_int64, C.c_int64, I, C.POINTER(SZ), C.POINTER(SZ)]),
         "runlora_exchange_create": (I, [P, I, I, C.c_int64, C.c_int64, C.c_int64, C.POINTER(P), C.POINTER(P), P,
@@ -165,11 +165,11 @@ def workspace_size(shape: Shape, fwd: int = 0, bwd: int = 0) -> int:
 
 
 class QuantizedWeight:
-    """A frozen W [k, m] stored as FP8 E4M3 bytes `q` with one fp32 `scale` per output
-    column (R18); `shape` is (k, m)."""
+    """A frozen W [k, m] stored as FP8 E4M3 bytes `q` with one power-of-two fp32 `scale` per
+    output column and their E5M2 diagonal `diag` [m, 128] (R18); `shape` is (k, m)."""
 
-    def __init__(self, q: torch.Tensor, scale: torch.Tensor):
-        self.q, self.scale = q, scale
+    def __init__(self, q: torch.Tensor, scale: torch.Tensor, diag: torch.Tensor):
+        self.q, self.scale, self.diag = q, scale, diag
 
     @property
     def shape(self):
@@ -278,20 +278,23 @@ class Handle:
         k, m = W.shape
         Wq = torch.empty(k, m, dtype=torch.uint8, device=W.device)
         scale = torch.empty(m, dtype=torch.float32, device=W.device)
-        _check(_lib.runlora_quantize_w_e4m3(self._h, k, m, _ptr(W), _ptr(Wq), _ptr(scale), _stream(self.device)),
-               "runlora_quantize_w_e4m3")
-        return QuantizedWeight(Wq, scale)
+        diag = torch.empty(m, 128, dtype=torch.uint8, device=W.device)
+        _check(_lib.runlora_quantize_w_e4m3(self._h, k, m, _ptr(W), _ptr(Wq), _ptr(scale), _ptr(diag),
+                                            _stream(self.device)), "runlora_quantize_w_e4m3")
+        return QuantizedWeight(Wq, scale, diag)
 
     def forward_wq(self, fwd, shape, X, Wq, A, B, Y, ws=None):
         ws = self.workspace(shape, True) if ws is None else ws
         _check(_lib.runlora_forward_wq(self._h, int(fwd), C.byref(shape), _ptr(X), _ptr(Wq.q), _ptr(Wq.scale),
-                                       _ptr(A), _ptr(B), _ptr(Y), _ptr(ws), ws.numel(), _stream(self.device)),
+                                       _ptr(Wq.diag), _ptr(A), _ptr(B), _ptr(Y), _ptr(ws), ws.numel(),
+                                       _stream(self.device)),
                "runlora_forward_wq")
 
     def backward_wq(self, bwd, shape, X, Wq, A, B, dY, dX, dA, dB, accumulate=False, ws=None):
         ws = self.workspace(shape, True) if ws is None else ws
         _check(_lib.runlora_backward_wq(self._h, int(bwd), C.byref(shape), _ptr(X), _ptr(Wq.q), _ptr(Wq.scale),
-                                        _ptr(A), _ptr(B), _ptr(dY), _ptr(dX), _ptr(dA), _ptr(dB), _DT[dA.dtype],
+                                        _ptr(Wq.diag), _ptr(A), _ptr(B), _ptr(dY), _ptr(dX), _ptr(dA), _ptr(dB),
+                                        _DT[dA.dtype],
                                         int(bool(accumulate)), _ptr(ws), ws.numel(), _stream(self.device)),
                "runlora_backward_wq")
 

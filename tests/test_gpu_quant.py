@@ -46,6 +46,16 @@ def test_quantize_and_dequantize_bit_exact(rl, c):
     q_o, s_o = Q.quantize_w(W.double().numpy())
     assert np.array_equal(qw.q.cpu().numpy(), q_o)
     assert np.array_equal(qw.scale.cpu().numpy(), s_o)
+    # the scale diagonal, decoded from the E5M2 definition (bias 15, 2 mantissa bits)
+    def e5m2(b):
+        e, mnt = (b >> 2) & 0x1F, b & 3
+        return (mnt / 4) * 2.0 ** -14 if e == 0 else (1 + mnt / 4) * 2.0 ** (e - 15)
+    D = qw.diag.cpu().numpy()
+    assert D.shape == (c.m, 128)
+    for j in range(c.m):
+        assert e5m2(int(D[j, j % 128])) == s_o[j], j
+        assert np.count_nonzero(D[j]) == 1
+
     # forward1 multiplies by W~ itself: the converter leaves it after the regular workspace
     shape = rl.make_shape(c.n, c.k, c.m, c.r, rl.BF16)
     ws = torch.zeros(rl.workspace_size_wq(shape), dtype=torch.uint8, device="cuda")
@@ -114,7 +124,7 @@ def test_wq_errors(rl):
     W = torch.randn(64, 12, device="cuda").to(torch.bfloat16)
     with pytest.raises(rl.RunLoRAError) as e:
         h.quantize_w(W)
-    assert e.value.status == 6  # m not a multiple of 8
+    assert e.value.status == 6  # m not a multiple of 16
     c = CASES[0]
     shape = rl.make_shape(c.n, c.k, c.m, c.r, rl.BF16)
     qw = h.quantize_w(torch.randn(c.k, c.m, device="cuda").to(torch.bfloat16))
@@ -127,10 +137,14 @@ def test_wq_errors(rl):
         h.forward_wq(1, shape, X, qw, A, B, Y, ws=small)
     assert e.value.status == 7
     # the 1-byte Wq needs 16-byte row strides: m a multiple of 16 (bf16 W only needs 8)
-    s8 = rl.make_shape(64, 256, 264, 8, rl.BF16)
-    q8 = h.quantize_w(torch.randn(256, 264, device="cuda").to(torch.bfloat16))
     with pytest.raises(rl.RunLoRAError) as e:
-        h.forward_wq(2, s8, X[:64, :256].contiguous(), q8, A[:256, :8].contiguous(), B[:8, :264].contiguous(),
+        h.quantize_w(torch.randn(256, 264, device="cuda").to(torch.bfloat16))
+    assert e.value.status == 6
+    s8 = rl.make_shape(64, 256, 264, 8, rl.BF16)
+    fake = rl.QuantizedWeight(torch.empty(256, 264, dtype=torch.uint8, device="cuda"),
+                              torch.ones(264, device="cuda"), torch.empty(264, 128, dtype=torch.uint8, device="cuda"))
+    with pytest.raises(rl.RunLoRAError) as e:
+        h.forward_wq(2, s8, X[:64, :256].contiguous(), fake, A[:256, :8].contiguous(), B[:8, :264].contiguous(),
                      torch.empty(64, 264, device="cuda", dtype=torch.bfloat16),
                      ws=torch.empty(rl.workspace_size_wq(s8), dtype=torch.uint8, device="cuda"))
     assert e.value.status == 6

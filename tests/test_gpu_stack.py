@@ -134,3 +134,50 @@ def test_stack_quantized_w_matches_oracle(problem):
     errs = _errors(y, xg, model.linears(), y_o, dx_o, grads_o)
     bad = {k: e for k, e in errs.items() if not e <= TOL}
     assert not bad, (bad, errs)
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_stack_token_shards_sum_to_p1(problem, P):
+    """C5 under token sharding (SURVEY §8(c) reading 14, reduced size): every layer is
+    row-wise in the tokens (R15: RMS norm, sums, the gate product), so P ranks that each run
+    n/P tokens through the stack hold partial adapter gradients whose sum is the P = 1
+    gradient (Eq. 3 sums over tokens).  The P ranks are emulated one after the other on this
+    GPU; their fp32 gradient buckets are summed by the exchange kernel
+    (runlora_allreduce_sum_f32, rank order) and compared with the P = 1 run of the same stack
+    and with the fp64 oracle."""
+    from paper_2312_03415_b200 import dp
+    from paper_2312_03415_b200 import runlora as rl
+    from paper_2312_03415_b200.stack import BucketedGradSync, LoRAStack, plan_model
+    weights, x, dy, _, _, grads_o = problem
+    model = LoRAStack.from_weights(weights, "cuda")
+    plan_model(model, N // P, rl.BY_FLOPS)
+    xs, dys = x.cuda(), dy.cuda()
+
+    def run(lo, hi):
+        sync = BucketedGradSync.for_model(model, bucket_bytes=8 << 20)
+        sync.begin_step(1)
+        model(xs[lo:hi].clone().requires_grad_(True)).backward(dys[lo:hi].contiguous())
+        sync.finish()
+        return sync
+
+    full = run(0, N)
+    shards = [run(*dp.shard_range(N, P, q)) for q in range(P)]
+    torch.cuda.synchronize()
+    h = rl.handle(0)
+    for bi, flat in enumerate(full.buckets):
+        out = torch.empty_like(flat)
+        h.allreduce_sum_f32([s.buckets[bi].data_ptr() for s in shards], out)
+        torch.cuda.synchronize()
+        e = rel_fro(_np(out), _np(flat))
+        assert e <= TOL, (bi, e)
+        assert e < 5e-3, (bi, e)  # healthy: only the bf16 activations of the shorter shards differ
+        flat.copy_(out)  # the sinks now view the summed gradients
+    where = {id(lin): (li, nm) for li, nm, lin in model.linears()}
+    errs = {}
+    for snk in full.sinks:  # views of the summed buckets
+        li, nm = where[id(snk.owner)]
+        errs[f"L{li}.{nm}.dA"] = rel_fro(_np(snk.dA), grads_o[li][nm][0])
+        errs[f"L{li}.{nm}.dB"] = rel_fro(_np(snk.dB), grads_o[li][nm][1])
+    assert len(errs) == 2 * len(model.linears())
+    bad = {k: e for k, e in errs.items() if not e <= TOL}
+    assert not bad, (bad, errs)
