@@ -16,7 +16,8 @@ from paper_2312_03415_b200 import runlora as rl  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--r", type=int, default=16)
 ap.add_argument("--plan", default="2,1")
-ap.add_argument("--steps", type=int, default=300)
+ap.add_argument("--steps", type=int, default=30)
+ap.add_argument("--blocks", type=int, default=20)
 a = ap.parse_args()
 c = synth.C2[a.r]
 d = {k: v.cuda() for k, v in synth.operands(c).items()}
@@ -42,8 +43,6 @@ def wq_step():
 
 
 def timed(fn):
-    for _ in range(20):
-        fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -54,14 +53,40 @@ def timed(fn):
     return e0.elapsed_time(e1) * 1e3 / a.steps
 
 
-t_b, t_q, t_b2, t_q2 = timed(bf16_step), timed(wq_step), timed(bf16_step), timed(wq_step)
-print(json.dumps({"workload": c.name, "plan": f"F{f}+B{b}", "bf16_W_us": (t_b + t_b2) / 2, "e4m3_W_us": (t_q + t_q2) / 2,
-                  "W_bytes_bf16": 2 * c.k * c.m, "W_bytes_e4m3": c.k * c.m + 4 * c.m}))
-h.profile_enable(True)
-h.profile_read(reset=True)
-for _ in range(50):
-    wq_step()
-torch.cuda.synchronize()
-prof = h.profile_read(reset=True)
-h.profile_enable(False)
-print(json.dumps({k: round(v[1] / v[0] * 1e3, 1) for k, v in prof.items()}))
+# alternating blocks (clock / power drift hits both alike), medians
+for fn in (bf16_step, wq_step):
+    for _ in range(20):
+        fn()
+tb, tq = [], []
+for _ in range(a.blocks):
+    tb.append(timed(bf16_step))
+    tq.append(timed(wq_step))
+import statistics as st
+print(json.dumps({"workload": c.name, "plan": f"F{f}+B{b}", "bf16_W_us": st.median(tb), "e4m3_W_us": st.median(tq),
+                  "e4m3_over_bf16": st.median([q / b_ for q, b_ in zip(tq, tb)]), "blocks": a.blocks,
+                  "steps_per_block": a.steps, "W_bytes_bf16": 2 * c.k * c.m,
+                  "W_bytes_e4m3": c.k * c.m + 4 * c.m + 128 * c.m}))
+if os.environ.get("RUNLORA_LTRACE"):  # per-launch in-step work (first ready -> last exit) + gap
+    import ctypes as C
+    import numpy as np
+    lib = rl._lib
+    lib.runlora_debug_ltrace.restype = C.c_int
+    lib.runlora_debug_kernel_name.restype = C.c_char_p
+    buf = np.zeros(8 * 4096, dtype=np.uint64)
+    kids = np.zeros(4096, dtype=np.int32)
+    args = (h._h, buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), kids.ctypes.data_as(C.POINTER(C.c_int)), 4096)
+    for name, fn in (("bf16", bf16_step), ("e4m3", wq_step), ("bf16", bf16_step), ("e4m3", wq_step)):
+        lib.runlora_debug_ltrace(*args)
+        for _ in range(50):
+            fn()
+        nrec = lib.runlora_debug_ltrace(*args)
+        rec = buf[: 8 * nrec].reshape(nrec, 8).astype(np.int64)
+        per = nrec // 50
+        rows = []
+        for pos in range(per):
+            idx = [s_ * per + pos for s_ in range(50)]
+            nm = lib.runlora_debug_kernel_name(int(kids[idx[0]])).decode()
+            wk = np.median([(rec[j, 4] - rec[j, 1]) / 1e3 for j in idx])
+            gp = np.median([(rec[j, 1] - rec[j - 1, 4]) / 1e3 for j in idx if j > 0])
+            rows.append(f"{nm}:{wk:.1f}+{gp:.1f}")
+        print(name, rows)
