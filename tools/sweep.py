@@ -47,8 +47,6 @@ def run(c, steps):
         h.forward(f, shape, d["X"], d["W"], d["A"], d["B"], Y, ws)
         h.backward(b, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], dX, dA, dB, ws=ws)
 
-    ms = timed(lambda: step(plan.fwd, plan.bwd), steps)
-    ms_flops = timed(lambda: step(pf.fwd, pf.bwd), steps)
     Xg = d["X"].clone().requires_grad_(True)
     Ag = d["A"].clone().requires_grad_(True)
     Bg = d["B"].clone().requires_grad_(True)
@@ -57,7 +55,14 @@ def run(c, steps):
         Xg.grad = Ag.grad = Bg.grad = None
         (Xg @ d["W"] + (Xg @ Ag) @ Bg).backward(d["dY"])
 
-    ms_def = timed(default, steps)
+    # alternating blocks of the three (clock and power drift hit all alike), medians
+    t = {"sel": [], "flops": [], "def": []}
+    for _ in range(3):
+        t["sel"].append(timed(lambda: step(plan.fwd, plan.bwd), steps))
+        t["flops"].append(timed(lambda: step(pf.fwd, pf.bwd), steps))
+        t["def"].append(timed(default, steps))
+    med = lambda v: sorted(v)[len(v) // 2]  # noqa: E731
+    ms, ms_flops, ms_def = med(t["sel"]), med(t["flops"]), med(t["def"])
     fl = plan.flops_fwd[plan.fwd] + plan.flops_bwd[plan.bwd]
     pd = plan.as_dict()
     return {"config": c.name, "n": c.n, "k": c.k, "m": c.m, "r": c.r,
