@@ -262,10 +262,11 @@ def main():
     from paper_2312_03415_b200 import dp
 
     rank = int(os.environ.get("RANK", "0"))
-    if world > 1:
-        # 6 main-GEMM stages leave shared memory for NCCL's kernels, which then co-reside
-        # with the dX GEMM that the adapter-gradient allreduce overlaps
-        os.environ.setdefault("RUNLORA_MAIN_STAGES", "6")
+    transport = os.environ.get("RUNLORA_DP_TRANSPORT", "nccl")
+    if world > 1 and transport == "nccl":
+        # the persistent dX GEMM fills every SM it runs on (registers and shared memory): two
+        # SMs left free let NCCL's allreduce kernel run beside it
+        os.environ.setdefault("RUNLORA_COMM_SMS", "2")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
@@ -286,9 +287,13 @@ def main():
     Y = torch.empty(n, m, dtype=torch.bfloat16, device=dev)
     dX = torch.empty(n, k, dtype=torch.bfloat16, device=dev)
     # DP exchange: NCCL allreduce (default) or the one-shot symmetric-memory kernel (opt-in)
-    sym = None
-    if world > 1 and args.backend == "nccl" and os.environ.get("RUNLORA_DP_TRANSPORT") == "symm":
+    # DP exchange: NCCL allreduce (default), the one-shot symmetric-memory kernel ("symm"), or the
+    # exchange fused into the dX GEMM launch ("fused", dp.FusedExchange) — both opt-in
+    sym = fused = None
+    if world > 1 and args.backend == "nccl" and transport == "symm":
         sym = dp.SymmetricAllreduce(k, r, m, dev, h)
+    if world > 1 and args.backend == "nccl" and transport == "fused":
+        fused = dp.FusedExchange(k, r, m, dev, h, multicast=os.environ.get("RUNLORA_DP_MULTICAST") == "1")
     g = sym.grads if sym is not None else dp.PackedAdapterGrads.create(k, r, m, dev)
     crit = {"flops": rl.BY_FLOPS, "time": rl.BY_TIME, "hybrid": rl.HYBRID}[args.criterion]
     if args.plan:
@@ -305,7 +310,9 @@ def main():
 
     def step():
         h.forward(fwd, shape, d["X"], d["W"], d["A"], d["B"], Y, ws)
-        if world > 1:
+        if fused is not None:
+            fused.backward(bwd, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], dX, g.dA, g.dB, ws=ws)
+        elif world > 1:
             work = dp.overlapped_backward(
                 lambda: h.backward_params(bwd, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], g.dA, g.dB, ws=ws),
                 lambda: h.backward_input(bwd, shape, d["X"], d["W"], d["A"], d["B"], d["dY"], dX, ws=ws),
@@ -535,7 +542,10 @@ def main():
                           "plan_times_us": plan.as_dict()["time_fwd_us"] | {f"B{v}": t for v, t in
                                                                            plan.as_dict()["time_bwd_us"].items()},
                           "flops_pick": f"F{plan.flops_fwd_pick}+B{plan.flops_bwd_pick}",
-                          "parallelism": f"dp{world} token-sharded, " + ("one-shot symmetric-memory allreduce" if sym is not None else "NCCL allreduce") + " of fp32 [dA|dB]",
+                          "parallelism": f"dp{world} token-sharded, " + (
+                              "one-shot symmetric-memory allreduce" if sym is not None else
+                              "exchange fused into the dX GEMM launch" if fused is not None else
+                              "NCCL allreduce") + " of fp32 [dA|dB]",
                           "l2": "inputs larger than L2: per-step working set X, dY, Y, dX 64 MiB each + W 32 MiB "
                                 "(288 MiB) > 126 MB L2"},
                "tflops": flops_step / (ms * 1e-3) / 1e12,

@@ -26,6 +26,7 @@ Ctx::Ctx(int device) : device_(device) {
   if (const char* e = getenv("RUNLORA_PDL")) pdl_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_L2PROMO_MN")) promo_mn_ = (CUtensorMapL2promotion)atoi(e);
   if (const char* e = getenv("RUNLORA_MAIN_STAGES")) main_stages_ = atoi(e) > 0 ? atoi(e) : 0;  // 0: all
+  if (const char* e = getenv("RUNLORA_COMM_SMS")) comm_sms_ = std::max(0, std::min(atoi(e), num_sms_ - 2)) & ~1;
   if (const char* e = getenv("RUNLORA_TMA_STORE_MAIN")) tma_store_main_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_MAIN_WIDE")) main_wide_ = atoi(e) != 0;
   if (const char* e = getenv("RUNLORA_WIDE_COST")) {

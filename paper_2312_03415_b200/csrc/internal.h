@@ -86,8 +86,8 @@ struct GemmReq {
   bool tail_diag;  // a2 = 128x128 identity, b2 read at the tile's own rows (see Prob)
   int a_policy;      // L2 policy of the A operand: 0 from a_stream_once, 1 normal, 2 evict-first
   bool tma_store;  // OUT_BF16 through the TMA-store epilogue (all problems of a launch alike)
-  bool overlaps_comm;  // the dX GEMM, which a data-parallel allreduce overlaps: runs on
-                       // RUNLORA_MAIN_STAGES (fewer ring stages leave shared memory for NCCL)
+  bool overlaps_comm;  // the dX GEMM, which a data-parallel allreduce overlaps: runs on the SMs
+                       // minus Ctx::comm_sms (and on RUNLORA_MAIN_STAGES ring stages)
   // in-kernel split-K fix-up (Prob::fixup): the last split of each output tile reduces the
   // slabs into fx_out (the ReduceJob semantics); counters zeroed by an earlier launch
   bool fixup;
@@ -137,12 +137,17 @@ class Ctx {
   bool main_wide() const { return main_wide_; }
   double wide_cost_a() const { return wide_cost_a_; }
   double wide_cost_e() const { return wide_cost_e_; }
-  std::map<std::tuple<int, int, int, int>, int>& wide_cache() { return wide_cache_; }
+  std::map<std::tuple<int, int, int, int, int>, int>& wide_cache() { return wide_cache_; }
   // main-GEMM pipeline stages (env RUNLORA_MAIN_STAGES; 0 = all that fit = 7).  6 stages
   // cost ~1 % in a step (the GEMM alone: 166.9 µs either way; 5: 169, 4: 181) and leave
   // 32 KB of shared memory per SM, so NCCL's kernels can co-reside with the dX GEMM that
   // the data-parallel allreduce overlaps (bench.py sets 6 when it runs more than one rank).
   int main_stages() const { return main_stages_; }
+  // SMs the dX GEMM (the one a data-parallel allreduce overlaps) leaves free for the
+  // collective's kernels (env RUNLORA_COMM_SMS, even, default 0): the persistent main GEMM
+  // holds ~63 K registers and ~225 KB of shared memory on every SM it runs on, so without free
+  // SMs an NCCL kernel cannot start before the GEMM ends
+  int comm_sms() const { return comm_sms_; }
   bool tma_store_wprime() const { return tma_store_wprime_; }
 
   // Encodes (or fetches from cache) a 2-D bf16 TMA descriptor with swz_bytes swizzle
@@ -182,8 +187,9 @@ class Ctx {
   bool tma_store_main_ = false;   // env RUNLORA_TMA_STORE_MAIN=1
   bool main_wide_ = true;
   double wide_cost_a_ = 1.66, wide_cost_e_ = 443.0;
-  std::map<std::tuple<int, int, int, int>, int> wide_cache_;  // (M, N, K, raster) -> rows_big
+  std::map<std::tuple<int, int, int, int, int>, int> wide_cache_;  // (M, N, K, raster, pairs) -> rows_big
   int main_stages_ = 0;
+  int comm_sms_ = 0;
   bool tma_store_wprime_ = true;  // env RUNLORA_TMA_STORE_WPRIME=0
   bool occ2_ = true;
   bool pdl_ = true;

@@ -40,7 +40,7 @@ cudaError_t launch_pdl(Ctx& ctx, void (*kern)(KArgs...), dim3 grid, dim3 block, 
 }
 
 template <int BN, int CG, int OCC = 1, int EPI = 0, int KS = 1>
-cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, GemmArgs& g, cudaStream_t s) {
+cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, GemmArgs& g, cudaStream_t s, int sms) {
   auto kern = tc_gemm_kernel<BN, CG, OCC, EPI, KS>;
   using TC = TileCfg<BN, CG, OCC, EPI, KS>;
   constexpr uint32_t smem_max = TC::SMEM_BYTES;
@@ -56,7 +56,7 @@ cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, GemmArgs& g, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
   }
-  int groups_max = ctx.num_sms() * OCC / CG;
+  int groups_max = sms * OCC / CG;  // persistent grid over the SMs this launch may use
   // debug (env RUNLORA_MAX_CTAS): cap the persistent grid of the non-main kernels, e.g. to
   // measure what a few SMs' worth of CTAs stream
   static const int max_ctas = getenv("RUNLORA_MAX_CTAS") ? atoi(getenv("RUNLORA_MAX_CTAS")) : 0;
@@ -95,11 +95,11 @@ cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, GemmArgs& g, cudaStream_t s) {
 }
 
 cudaError_t dispatch_tc(Ctx& ctx, int bn_max, int cg, bool occ2, bool tma_store, const Tmaps& tm, GemmArgs& g,
-                        cudaStream_t s) {
+                        cudaStream_t s, int sms) {
   if (tma_store) {
-    if (cg == 1 && bn_max == 256) return run_tc<256, 1, 1, 3>(ctx, tm, g, s);
-    if (cg == 2 && bn_max == 256) return run_tc<256, 2, 1, 3>(ctx, tm, g, s);
-    if (cg == 2 && bn_max == 512) return run_tc<512, 2, 1, 3>(ctx, tm, g, s);
+    if (cg == 1 && bn_max == 256) return run_tc<256, 1, 1, 3>(ctx, tm, g, s, sms);
+    if (cg == 2 && bn_max == 256) return run_tc<256, 2, 1, 3>(ctx, tm, g, s, sms);
+    if (cg == 2 && bn_max == 512) return run_tc<512, 2, 1, 3>(ctx, tm, g, s, sms);
     return cudaErrorNotSupported;
   }
   if (cg == 2) {
@@ -108,29 +108,29 @@ cudaError_t dispatch_tc(Ctx& ctx, int bn_max, int cg, bool occ2, bool tma_store,
     // (8192x4096x4096: 180 vs 197 µs) and neutral for K-major operands (168 µs both).
     static const int ks_env = getenv("RUNLORA_MAIN_KS") ? atoi(getenv("RUNLORA_MAIN_KS")) : 0;
     const bool ks2 = ks_env ? ks_env == 2 : (g.p[0].a_mn || g.p[0].b_mn);
-    if (bn_max == 512) return run_tc<512, 2>(ctx, tm, g, s);
-    if (bn_max == 256 && ks2) return run_tc<256, 2, 1, 0, 2>(ctx, tm, g, s);
-    if (bn_max == 256) return run_tc<256, 2>(ctx, tm, g, s);
-    if (bn_max == 128) return run_tc<128, 2>(ctx, tm, g, s);
+    if (bn_max == 512) return run_tc<512, 2>(ctx, tm, g, s, sms);
+    if (bn_max == 256 && ks2) return run_tc<256, 2, 1, 0, 2>(ctx, tm, g, s, sms);
+    if (bn_max == 256) return run_tc<256, 2>(ctx, tm, g, s, sms);
+    if (bn_max == 128) return run_tc<128, 2>(ctx, tm, g, s, sms);
     return cudaErrorInvalidValue;
   }
   if (occ2) {
     switch (bn_max) {
-      case 16: return run_tc<16, 1, 2>(ctx, tm, g, s);
-      case 32: return run_tc<32, 1, 2>(ctx, tm, g, s);
-      case 48: return run_tc<48, 1, 2>(ctx, tm, g, s);
-      case 64: return run_tc<64, 1, 2>(ctx, tm, g, s);
-      case 128: return run_tc<128, 1, 2>(ctx, tm, g, s);
+      case 16: return run_tc<16, 1, 2>(ctx, tm, g, s, sms);
+      case 32: return run_tc<32, 1, 2>(ctx, tm, g, s, sms);
+      case 48: return run_tc<48, 1, 2>(ctx, tm, g, s, sms);
+      case 64: return run_tc<64, 1, 2>(ctx, tm, g, s, sms);
+      case 128: return run_tc<128, 1, 2>(ctx, tm, g, s, sms);
       default: break;
     }
   }
   switch (bn_max) {
-    case 16: return run_tc<16, 1>(ctx, tm, g, s);
-    case 32: return run_tc<32, 1>(ctx, tm, g, s);
-    case 48: return run_tc<48, 1>(ctx, tm, g, s);
-    case 64: return run_tc<64, 1>(ctx, tm, g, s);
-    case 128: return run_tc<128, 1>(ctx, tm, g, s);
-    case 256: return run_tc<256, 1>(ctx, tm, g, s);
+    case 16: return run_tc<16, 1>(ctx, tm, g, s, sms);
+    case 32: return run_tc<32, 1>(ctx, tm, g, s, sms);
+    case 48: return run_tc<48, 1>(ctx, tm, g, s, sms);
+    case 64: return run_tc<64, 1>(ctx, tm, g, s, sms);
+    case 128: return run_tc<128, 1>(ctx, tm, g, s, sms);
+    case 256: return run_tc<256, 1>(ctx, tm, g, s, sms);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -429,7 +429,8 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
   // 2 CTAs per SM for the HBM-bound rank-r kernels; at 128 columns only for the token
   // reductions (r = 128: 42.6 -> 31.0 µs; the projections lost 38 -> 45 µs to the shallower ring)
   const bool occ2 = ctx.occ2() && reqs[0].a_stream_once && (bn_max <= 64 || reqs[0].kid == KID_GEMM_TOKRED);
-  cudaError_t e = dispatch_tc(ctx, bn_max, cg, occ2, tma_store, tm, g, s);
+  const int sms = ctx.num_sms() - ((reqs[0].kid == KID_GEMM_MAIN && reqs[0].overlaps_comm) ? ctx.comm_sms() : 0);
+  cudaError_t e = dispatch_tc(ctx, bn_max, cg, occ2, tma_store, tm, g, s, sms);
   ctx.launch_end(s);
   if (e == cudaSuccess && nfb > 0) e = launch_splitk_reduce(ctx, fallback, nfb, s);
   if (e != cudaSuccess && err) *err = std::string("tc_gemm launch: ") + cudaGetErrorString(e);

@@ -627,13 +627,13 @@ WideSplit wide_split(Ctx& c, const GemmReq& q) {
   if (!c.main_wide() || q.cg != 2 || q.a_mn || q.b_mn || q.splits > 1 || q.out_mode != OUT_BF16) return w;
   const int G = raster_rows(q);
   const int K = q.K1 + q.K2;
-  const auto key = std::make_tuple(q.M, q.N, K, G);
+  const int pairs = (c.num_sms() - (q.overlaps_comm ? c.comm_sms() : 0)) / 2;  // launch_tc_gemm's grid
+  const auto key = std::make_tuple(q.M, q.N, K, G, pairs);
   auto& cache = c.wide_cache();
   if (auto it = cache.find(key); it != cache.end()) {
     w.rows_big = it->second;
     return w;
   }
-  const int pairs = c.num_sms() / 2;
   const int mt = (q.M + 255) / 256;
   const int ntb = (q.N + 511) / 512, nts = (q.N + 255) / 256;
   const bool ragged = (int64_t)ntb * 512 - q.N >= 256;  // last 512-wide column tile has one half

@@ -152,3 +152,36 @@ def test_wide_outputs_stay_in_bounds(rl):
     for buf, n_in in ((ybuf, c.n * c.m), (xbuf, c.n * c.k)):
         assert bool((buf[:pad] == sentinel.item()).all()) and bool((buf[pad + n_in:] == sentinel.item()).all())
         assert not bool((buf[pad:pad + n_in] == sentinel.item()).any())  # every element written
+
+
+def test_comm_sms_leave_sms_free_for_the_collective(tmp_path):
+    """RUNLORA_COMM_SMS = 2 (bench.py sets it under NCCL data parallelism): the dX GEMM — the
+    launch the adapter-gradient allreduce overlaps — runs its persistent grid on 146 of the
+    148 SMs (the 512/256-wide split re-planned for 73 pairs), the Y GEMM keeps all of them,
+    and the outputs stay parity-green (tile order changes the K direction of some tiles,
+    so they are not bit-identical)."""
+    import os
+    import re
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "child.py"
+    script.write_text(_CHILD.format(root=root))
+    outs, grids = [], []
+    for cs in ("", "2"):
+        env = dict(os.environ)
+        env.pop("RUNLORA_COMM_SMS", None)
+        env.pop("RUNLORA_MAIN_STAGES", None)
+        env["RUNLORA_DEBUG_LAUNCH"] = "1"
+        if cs:
+            env["RUNLORA_COMM_SMS"] = cs
+        f = tmp_path / f"out{cs or 'default'}.pt"
+        p = subprocess.run([sys.executable, str(script), str(f)], env=env, capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs.append(torch.load(f))
+        grids.append([int(m.group(1)) for m in re.finditer(r"tc_gemm<512,2,[^>]*> grid (\d+)", p.stderr)])
+    assert grids[0] == [148, 148] and grids[1] == [148, 146], grids
+    for k in ("Y", "dA", "dB"):
+        assert torch.equal(outs[0][k], outs[1][k]), k  # the Y GEMM and the adapter gradients are untouched
+    d = (outs[0]["dX"].double() - outs[1]["dX"].double()).norm() / outs[0]["dX"].double().norm()
+    assert d < 1e-3, d
