@@ -166,7 +166,9 @@ def test_comm_sms_leave_sms_free_for_the_collective(tmp_path):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     script = tmp_path / "child.py"
-    script.write_text(_CHILD.format(root=root))
+    # enough units that the persistent grid is bounded by the SMs (C4 per-rank size at P = 4)
+    script.write_text(_CHILD.format(root=root).replace('synth.case("wide_w1", 0, 40, 3000, 2048, 3304, 16, "bf16")',
+                                                      'synth.case("comm", 0, 42, 8192, 2048, 2048, 16, "bf16")'))
     outs, grids = [], []
     for cs in ("", "2"):
         env = dict(os.environ)
