@@ -64,7 +64,7 @@ cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, GemmArgs& g, cudaStream_t s, int s
   const int groups = g.total_units < groups_max ? g.total_units : groups_max;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(groups * CG);
-  cfg.blockDim = dim3(kGemmThreads);
+  cfg.blockDim = dim3(TC::THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
@@ -87,7 +87,7 @@ cudaError_t run_tc(Ctx& ctx, const Tmaps& tm, GemmArgs& g, cudaStream_t s, int s
   static const bool dbg_launch = getenv("RUNLORA_DEBUG_LAUNCH") != nullptr;
   if (dbg_launch) {
     int occ = -1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGemmThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TC::THREADS, smem);
     fprintf(stderr, "[runlora] tc_gemm<%d,%d,%d,%d,%d> grid %d smem %u occupancy/SM %d units %d: %s\n", BN, CG, OCC,
             EPI, KS, groups * CG, smem, occ, g.total_units, cudaGetErrorString(e));
   }

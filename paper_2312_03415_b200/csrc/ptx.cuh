@@ -279,6 +279,16 @@ __device__ __forceinline__ void reg_fence32(uint32_t (&v)[32]) {
 }
 
 // 32 lanes x 32 consecutive 32-bit columns: thread t gets row (lane_base+t), cols [col, col+32).
+// Warp-group register reallocation (all 128 threads of the warp group execute it).
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "

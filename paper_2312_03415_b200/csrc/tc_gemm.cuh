@@ -122,7 +122,7 @@ struct GemmArgs {
   int total_units;
   int dbg;  // 0 normal; 1: no TMA (MMA-only); 2: no MMA (TMA-only); 3: as 1 + no stores; 4: as 1 + no epilogue;
             // 5: A loads only (MMA on stale B); 6: B loads only (stale A); 7: A loads on even
-            // k-blocks only (75 % of the TMA bytes)
+            // k-blocks only (75 % of the TMA bytes); 8: 512-wide tiles read TMEM but store nothing
   // Debug timeline (RUNLORA_TRACE): per unit u, trace[8u + {0: producer start, 2: last load
   // issued, 3: epilogue done, 4: CTA, 5: problem}] (%globaltimer ns).
   unsigned long long* trace;
@@ -147,7 +147,8 @@ constexpr int kStgBufs = 4;  // EPI = 3 staging tiles per epilogue warp (a 256-w
 constexpr int kBM = 128;  // rows per CTA
 constexpr int kMaxFixups = 64;  // split fix-ups one CTA can defer to the end of its unit loop
 constexpr int kBK = 64;
-constexpr int kGemmThreads = 256;
+constexpr int kWideRegsLow = 120;   // setmaxnreg of the 512-wide kernel's warp groups:
+constexpr int kWideRegsHigh = 184;  // 128 x 104 + 256 x 200 = 384 x 168 (launch allocation)
 
 // OCC = CTAs per SM (2 for the HBM-bound rank-r kernels: twice the TMA requests in flight).
 // EPI = 3: TMA-store epilogue (bf16 tile staged per warp in swizzled smem).
@@ -159,10 +160,17 @@ struct TileCfg {
   static constexpr uint32_t A_BYTES = KS * A_ATOM;
   static constexpr uint32_t B_BYTES = KS * B_ATOM;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  // EPI = 3: per epilogue warp kStgBufs 32-row x 64-column bf16 staging tiles (128B swizzle)
-  // (2 for 512-wide tiles, whose 4 ring stages of 48 KB leave 32 KB)
-  static constexpr int STG_BUFS = BN_MAX > 256 ? 2 : kStgBufs;
-  static constexpr uint32_t STG_BYTES = EPI == 3 ? 4 * STG_BUFS * 4096 : 0;
+  // Epilogue warps: 4 (one per TMEM lane quarter), or 8 for the 512-wide TMA-store kernel —
+  // two per lane quarter, each holding 128 columns of both accumulator slots in registers
+  // (bf16 pairs, 128 registers per thread), so the whole tile leaves TMEM at TMEM-read speed
+  // and its stores overlap the next tile's mainloop (warp-group register split: setmaxnreg).
+  static constexpr bool WIDE_HOLD = BN_MAX > 256 && EPI == 3;
+  static constexpr int EPI_WARPS = WIDE_HOLD ? 8 : 4;
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
+  // EPI = 3: per epilogue warp STG_BUFS 32-row x 64-column bf16 staging tiles (128B swizzle)
+  // (1 for the 512-wide kernel, whose 4 ring stages of 48 KB leave 32 KB for 8 warps)
+  static constexpr int STG_BUFS = WIDE_HOLD ? 1 : kStgBufs;
+  static constexpr uint32_t STG_BYTES = EPI == 3 ? EPI_WARPS * STG_BUFS * 4096 : 0;
   // up to ~225 KB of the 227 KB opt-in smem per SM (7 stages for the 256x256 pair tiles)
   static constexpr int STAGES_RAW = ((OCC == 1 ? 225 : 110) * 1024 - STG_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
@@ -434,7 +442,7 @@ __device__ __forceinline__ void stage_store_packed(const uint32_t (&pk)[32], uin
 // EPI = 0: epilogue stores from registers; EPI = 3: TMA-store epilogue (plain bf16 outputs).
 // KS: 64-wide K atoms per pipeline stage (TileCfg).
 template <int BN_MAX, int CG, int OCC = 1, int EPI = 0, int KS = 1>
-__global__ void __launch_bounds__(kGemmThreads, OCC)
+__global__ void __launch_bounds__(TileCfg<BN_MAX, CG, OCC, EPI, KS>::THREADS, OCC)
     tc_gemm_kernel(const __grid_constant__ Tmaps tm, const __grid_constant__ GemmArgs g) {
   using C = TileCfg<BN_MAX, CG, OCC, EPI, KS>;
   // features compiled only where they are used, so the main GEMMs' code (and its MMA issue
@@ -491,7 +499,7 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4 * CG);
+      mbar_init(&tempty[a], C::EPI_WARPS * CG);
     }
     fence_mbar_init();
   }
@@ -509,7 +517,11 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
   if (ctrace && threadIdx.x == 0) ctrace[1] = globaltimer();
   if (threadIdx.x == 0) ltrace_mark(g.ltrace, 1);
 
-  if (warp == 0) {
+  // Roles: warp group 0 = TMA producer (warp 0), MMA issuer (warp 1), side jobs (warps 2-3);
+  // the other warps = epilogue.  The bodies are inlined lambdas so that the 512-wide
+  // TMA-store kernel can wrap them in its warp-group register split while every other
+  // kernel keeps the plain dispatch chain (its code generation unchanged).
+  auto run_producer = [&]() __attribute__((always_inline)) {
     // ------------------------------------------------------------ TMA producer
     // The whole warp runs the loop (warp-uniform values); one elected lane issues.
     int stage = 0;
@@ -615,7 +627,8 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       }
       if (g.trace && lane == 0) g.trace[8 * u + 2] = globaltimer();
     }
-  } else if (warp == 1 && leader) {
+  };
+  auto run_mma = [&]() __attribute__((always_inline)) {
     // ------------------------------------------------------------- MMA issuer
     // Whole warp in the loop so descriptors live in uniform registers; one elected
     // lane issues tcgen05.mma / tcgen05.commit.
@@ -739,7 +752,8 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       }
       sc += nh;
     }
-  } else if (kSide && (warp == 2 || warp == 3) && g.nside > 0) {
+  };
+  auto run_side = [&]() __attribute__((always_inline)) {
     // ----------------------------------------------- side job of the idle warps
     if (g.xdesc) {
       XSlabs S;
@@ -757,9 +771,13 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
     } else {
       side_reduce(g, (long long)blockIdx.x * 64 + (threadIdx.x - 64), (long long)gridDim.x * 64);
     }
-  } else if (warp >= 4) {
+  };
+  auto run_epilogue = [&]() __attribute__((always_inline)) {
     // --------------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int ew = warp - 4;  // epilogue warp: staging buffers; with 8 warps, ew >> 2 = column half
+    constexpr int kEpiStep = C::EPI_WARPS / 4;
+    const int hp = C::EPI_WARPS == 8 ? ew >> 2 : 0;
     int it = 0;
     int st_it = 0;  // EPI = 3: TMA stores issued by this warp
     int sc = 0;     // accumulator slots consumed (same sequence as the MMA issuer)
@@ -774,56 +792,47 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
       const int n0 = t.n_blk * p.bn;
       const int row = (g.dbg == 3) ? 0x7fffffff : m0 + q * 32 + lane;
       const int nh = BN_MAX > SLOT_W ? unit_halves(p, t.n_blk, SLOT_W) : 1;
-      if constexpr (BN_MAX > SLOT_W && EPI == 3) {
+      if constexpr (C::WIDE_HOLD) {
         if (nh == 2 && g.dbg != 4) {
-          // 512-wide tile: slot A (tile columns [0, 256)) is read into registers as bf16 and
-          // released at once, so the next tile's MMA 0 starts while slot B (columns
-          // [256, 512)) is staged and stored; slot A's rows are stored last.
+          // 512-wide tile, 8 warps: this warp reads columns [128 hp, +128) of slot A (tile
+          // columns [0, 256)) and of slot B (tile columns [256, 512)) into registers as bf16,
+          // releasing each slot as soon as it is read; the stores follow while the next
+          // tile's MMAs run.
           const int sA = sc & 1, sB = sA ^ 1;
-          uint8_t* stg = smem + STAGES * C::STAGE_BYTES + q * (C::STG_BUFS * 4096);
+          uint8_t* stg = smem + STAGES * C::STAGE_BYTES + ew * (C::STG_BUFS * 4096);
           const CUtensorMap* dmap = &tm.m[t.prob][4];
-          const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-          uint32_t held[4][32];  // 4 chunks x 64 columns, bf16 pairs
-          mbar_wait(&tfull[sA], (sA ? use1 : use0) & 1);
-          tc_fence_after();
+          const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + (uint32_t)(128 * hp);
+          uint32_t held[4][32];  // [slot A c0, c1, slot B c0, c1] x 64 columns, bf16 pairs
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int sl = h ? sB : sA;
+            mbar_wait(&tfull[sl], (sl ? use1 : use0) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              uint32_t v[2][32];
+              tmem_ld_32x32b_x32(t_lane + (uint32_t)(sl * SLOT_W + 64 * c), v[0]);
+              tmem_ld_32x32b_x32(t_lane + (uint32_t)(sl * SLOT_W + 64 * c + 32), v[1]);
+              tmem_ld_wait();
+              reg_fence32(v[0]);
+              reg_fence32(v[1]);
+#pragma unroll
+              for (int x = 0; x < 32; ++x)
+                held[2 * h + c][x] = pack_bf16x2(__uint_as_float(v[x >> 4][2 * (x & 15)]),
+                                                 __uint_as_float(v[x >> 4][2 * (x & 15) + 1]));
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote<CG>(&tempty[sl], 0);
+            if (sl) ++use1;
+            else ++use0;
+          }
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            uint32_t v[2][32];
-            tmem_ld_32x32b_x32(t_lane + (uint32_t)(sA * SLOT_W + 64 * c), v[0]);
-            tmem_ld_32x32b_x32(t_lane + (uint32_t)(sA * SLOT_W + 64 * c + 32), v[1]);
-            tmem_ld_wait();
-            reg_fence32(v[0]);
-            reg_fence32(v[1]);
-#pragma unroll
-            for (int x = 0; x < 32; ++x)
-              held[c][x] = pack_bf16x2(__uint_as_float(v[x >> 4][2 * (x & 15)]), __uint_as_float(v[x >> 4][2 * (x & 15) + 1]));
+            const int col = n0 + (c >> 1) * SLOT_W + 128 * hp + 64 * (c & 1);
+            if (col < p.N && g.dbg != 3 && g.dbg != 8)
+              stage_store_packed<C::STG_BUFS>(held[c], stg, st_it, lane, dmap, col, m0 + q * 32);
           }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_remote<CG>(&tempty[sA], 0);
-          if (sA) ++use1;
-          else ++use0;
-          mbar_wait(&tfull[sB], (sB ? use1 : use0) & 1);
-          tc_fence_after();
-#pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            if (n0 + SLOT_W + 64 * c >= p.N) break;  // warp-uniform
-            uint32_t v[2][32];
-            tmem_ld_32x32b_x32(t_lane + (uint32_t)(sB * SLOT_W + 64 * c), v[0]);
-            tmem_ld_32x32b_x32(t_lane + (uint32_t)(sB * SLOT_W + 64 * c + 32), v[1]);
-            tmem_ld_wait();
-            reg_fence32(v[0]);
-            reg_fence32(v[1]);
-            stage_store_chunk<C::STG_BUFS>(v, stg, st_it, lane, dmap, n0 + SLOT_W + 64 * c, m0 + q * 32);
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_remote<CG>(&tempty[sB], 0);
-          if (sB) ++use1;
-          else ++use0;
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (n0 + 64 * c < p.N) stage_store_packed<C::STG_BUFS>(held[c], stg, st_it, lane, dmap, n0 + 64 * c, m0 + q * 32);
           sc += 2;
           if (g.trace && threadIdx.x == 4 * 32) g.trace[8 * u + 3] = globaltimer();
           continue;
@@ -842,11 +851,11 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
           // writes; rows >= M / cols >= N are clipped by the tensor map bounds).  64-column
           // chunks, STG_BUFS staging tiles per warp: a buffer is reused only after the store
           // issued STG_BUFS chunks earlier has finished reading it.
-          uint8_t* stg = smem + STAGES * C::STAGE_BYTES + q * (C::STG_BUFS * 4096);
+          uint8_t* stg = smem + STAGES * C::STAGE_BYTES + ew * (C::STG_BUFS * 4096);
           const int nch = min(bw, p.N - nc + 63) / 64;  // 64-column chunks inside N
           const CUtensorMap* dmap = &tm.m[t.prob][4];
 #pragma unroll 1
-          for (int i = 0; i < nch; ++i) {
+          for (int i = hp; i < nch; i += kEpiStep) {
             uint32_t v[2][32];
             tmem_ld_32x32b_x32(t_row + 64 * i, v[0]);
             tmem_ld_32x32b_x32(t_row + 64 * i + 32, v[1]);
@@ -948,6 +957,25 @@ __global__ void __launch_bounds__(kGemmThreads, OCC)
         }
       }
     }
+  };
+  if constexpr (C::WIDE_HOLD) {
+    // 384 threads x 168 registers: warp group 0 gives registers to the two epilogue warp
+    // groups (held tile + staging); the reallocation opens each branch so that the compiler
+    // allocates each region against its own limit
+    if (warp < 4) {
+      setmaxnreg_dec<kWideRegsLow>();
+      if (warp == 0) run_producer();
+      else if (warp == 1 && leader) run_mma();
+      else if (kSide && (warp == 2 || warp == 3) && g.nside > 0) run_side();
+    } else {
+      setmaxnreg_inc<kWideRegsHigh>();
+      run_epilogue();
+    }
+  } else {
+    if (warp == 0) run_producer();
+    else if (warp == 1 && leader) run_mma();
+    else if (kSide && (warp == 2 || warp == 3) && g.nside > 0) run_side();
+    else if (warp >= 4) run_epilogue();
   }
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync();
