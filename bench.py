@@ -40,6 +40,7 @@ METRIC = "LoRA-linear fwd+bwd tokens/s, tensor-pipe util, speedup vs default XW+
 UNIT = "tokens/s"
 CAPTION = "synthetic: seeded i.i.d. Gaussian operands with BASELINE.json's laws (no dataset/weights)"
 ORACLE_SLICE = 1024  # tokens per oracle slice (cpu_baseline and the reference arm alike)
+E2E_SETS = 3  # steps in flight in the e2e leg (own streams, device buffers and workspaces)
 
 
 def _peaks():
@@ -435,12 +436,15 @@ def main():
     # ---------------- end to end through the C ABI with host buffers
     # Every step: H2D of its X, dY from pinned host memory, forward + backward (+ the DP
     # allreduce through the exchange hook at N > 1), D2H of dA, dB and of Y, dX
-    # (runlora_step_host).  Two steps are in flight on two streams with their own device
-    # buffers and workspaces, so one step's PCIe copies overlap the other's kernels.
+    # (runlora_step_host).  Three steps are in flight on three streams with their own device
+    # buffers and workspaces: a stream runs its step's H2D, kernels and D2H in order, so with
+    # three of them one step's inputs stream in while another's outputs stream out and a third
+    # computes — both PCIe directions stay busy (tools/pcie_probe.py: 128 MiB each way take
+    # 2.7 ms concurrently, the floor of a C2 step's 256 MiB of copies).
     hx = ops["X"].pin_memory()
     hdy = ops["dY"].pin_memory()
     sets = []
-    for j in range(2):
+    for j in range(E2E_SETS):
         gj = dp.PackedAdapterGrads.create(k, r, m, dev)
         devj = {"W": d["W"], "A": d["A"], "B": d["B"],
                 "X": torch.empty_like(d["X"]), "dY": torch.empty_like(d["dY"]),
@@ -456,7 +460,7 @@ def main():
         for st_j, *_ in sets:
             st_j.wait_stream(cur)
         for i in range(K):
-            st_j, devj, hostj, gj, wsj = sets[i % 2]
+            st_j, devj, hostj, gj, wsj = sets[i % len(sets)]
             hj = hostj if outputs else {kk: v for kk, v in hostj.items() if kk not in ("Y", "dX")}
             with torch.cuda.stream(st_j):
                 h.step_host(shape, fwd, bwd, hj, devj, rl.F32, ws=wsj,
@@ -464,7 +468,7 @@ def main():
         for st_j, *_ in sets:
             cur.wait_stream(st_j)
 
-    e2e_steps = max(4, args.steps // 4)
+    e2e_steps = max(12, args.steps)  # long enough that the 3-deep pipeline fill and drain are a small share
     res = {}
     for outputs in (True, False):
         e2e_run(max(4, args.warmup // 2), outputs)
@@ -474,7 +478,8 @@ def main():
            "h2d_bytes_per_step": xb + yb, "d2h_bytes_per_step": k * r * 4 + r * m * 4 + yb + xb,
            "note": "runlora_step_host every step: H2D X, dY from pinned host; forward; backward"
                    + ("; NCCL allreduce of fp32 [dA|dB] through the exchange hook" if world > 1 else "")
-                   + "; D2H of Y, dX (bf16) and dA, dB (fp32). 2 steps in flight on 2 streams (PCIe-bound)",
+                   + f"; D2H of Y, dX (bf16) and dA, dB (fp32). {E2E_SETS} steps in flight on {E2E_SETS} streams "
+                     "(PCIe-bound)",
            "grads_only": {"value": world * n / (res[False] * 1e-3), "ms_per_step": res[False],
                           "d2h_bytes_per_step": k * r * 4 + r * m * 4,
                           "note": "same, but only dA, dB come back (Y, dX stay resident)"}}

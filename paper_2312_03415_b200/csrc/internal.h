@@ -186,7 +186,7 @@ class Ctx {
   void* identity_ = nullptr;
   bool tma_store_main_ = false;   // env RUNLORA_TMA_STORE_MAIN=1
   bool main_wide_ = true;
-  double wide_cost_a_ = 1.66, wide_cost_e_ = 443.0;
+  double wide_cost_a_ = 1.72, wide_cost_e_ = 41.0;
   std::map<std::tuple<int, int, int, int, int>, int> wide_cache_;  // (M, N, K, raster, pairs) -> rows_big
   int main_stages_ = 0;
   int comm_sms_ = 0;

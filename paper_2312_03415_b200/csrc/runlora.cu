@@ -599,14 +599,15 @@ runlora_status_t wprime_q(Ctx& c, const runlora_shape_t& s, const QW& w, const v
 // ------------------------------------------------------------ 512-wide main-GEMM tiles
 // A 256x512 pair tile (two N = 256 MMAs per k-step sharing the A tile) moves 25 % fewer TMA
 // bytes per FLOP than a 256x256 one, and the main GEMM's time tracks those bytes (DESIGN.md
-// §5); but its 512 accumulator columns leave no second TMEM buffer, so its epilogue (one
-// burst of output writes per round) is exposed, and big tiles quantise coarsely on 74 pairs
-// (C2: 256 tiles = 3.46 rounds).  So output rows [0, rows_big) run as 512-wide tiles and
+// §5); its 512 accumulator columns leave no second TMEM buffer (the kernel's 8 epilogue
+// warps read the whole tile into registers and release TMEM before storing), and big tiles
+// quantise coarsely on 74 pairs (C2: 256 tiles = 3.46 rounds).  So output rows [0, rows_big) run as 512-wide tiles and
 // the rest as 256-wide ones in the same launch (two problems).  rows_big minimises the
 // busiest pair's summed unit cost under the kernel's static round-robin assignment (unit u
 // -> pair u mod 74).  Cost of a 512-wide tile in 256-wide tile times: a + e / K, fitted to
-// gemm_bench runs at K = 2048 / 4096 (1.87 / 1.77: a = 1.66, e = 443 — the exposed epilogue,
-// ~2.8 µs, against a 256-wide tile's ~6.4 ns per K).  Cached per shape.
+// gemm_bench runs at 131072 x 2048 x K, K = 2048 / 4096 / 8192 (1.744 / 1.741 / 1.729: a =
+// 1.72, e = 41 — with the tile held in registers the epilogue is nearly hidden; before, the
+// exposed epilogue made it 1.87 at K = 2048).  Cached per shape.
 struct WideSplit {
   int rows_big;  // multiple of 256; 0 = no 512-wide tiles
   double cost, cost_small_only;
