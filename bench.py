@@ -696,7 +696,10 @@ def c5_stack(args, rl, dist, dev, local, world, rank, timed):
            "tokens_per_rank": per_rank, "micro_batches": micro, "micro_batch_tokens": mb,
            "plans": {f"{k}x{m}": f"F{int(p.fwd)}+B{int(p.bwd)}" for (k, m, _), p in plans.items()},
            "steps": args.c5_steps, "warmup": w, "ms_per_step": ms, "tokens_per_s": n_glob / (ms * 1e-3),
-           "parallelism": f"dp{world} token-sharded, bucketed NCCL allreduce of fp32 adapter grads"}
+           "parallelism": f"dp{world} token-sharded, bucketed NCCL allreduce of fp32 adapter grads",
+           "wprime_reuse": all(lin.wcache is not None for _, _, lin in model.linears()),
+           "note": "forward2's W'ᵀ built once per step per linear and reused by the micro-batches "
+                   "(runlora_wprime_t + runlora_forward_wprime, lora.WPrimeCache)"}
     if not args.no_default_chain:
         base = LoRAStack([LoRALayer({nm: DefaultLinear(L.lin[nm]) for nm in LINEARS}) for L in model.layers]).to(dev)
         if world > 1:

@@ -183,6 +183,25 @@ runlora_status_t runlora_backward_input(runlora_handle_t h, int bwd, const runlo
                                         const void* dY, void* dX, void* workspace, size_t ws_bytes,
                                         void* stream);
 
+/* forward2 in two halves (Eq. 2; "forward2" computes X(W + AB)):
+ *   runlora_wprime_t:       Wpt = (W + A·B)ᵀ, [m, k] bf16 row-major (fp32 accumulation, one
+ *                           rounding; the identity-tail GEMM forward2 itself runs)
+ *   runlora_forward_wprime: Y = X·W' reading Wpt (the main GEMM forward2 itself runs)
+ * Together they are runlora_forward(2) bit for bit.  For callers that reuse W' while A and B
+ * are unchanged — the micro-batches of one gradient-accumulation step — and so build it once
+ * per step instead of once per call; keeping Wpt valid (rebuilding it after A or B change) is
+ * the caller's job.  Wpt: caller device memory, m·k bf16, 16-byte aligned.  bf16 shapes only
+ * (else RUNLORA_ERR_DTYPE).  runlora_wprime_t needs no workspace; runlora_forward_wprime needs
+ * runlora_workspace_size(s, 2, 0) bytes.  runlora_wprime_t_wq: the same from a quantized W
+ * (Wq, scale, diag below; m a multiple of 16).  Asynchronous on `stream`. */
+runlora_status_t runlora_wprime_t(runlora_handle_t h, const runlora_shape_t* s, const void* W, const void* A,
+                                  const void* B, void* Wpt, void* stream);
+runlora_status_t runlora_wprime_t_wq(runlora_handle_t h, const runlora_shape_t* s, const void* Wq,
+                                     const float* scale, const void* diag, const void* A, const void* B, void* Wpt,
+                                     void* stream);
+runlora_status_t runlora_forward_wprime(runlora_handle_t h, const runlora_shape_t* s, const void* X, const void* Wpt,
+                                        void* Y, void* workspace, size_t ws_bytes, void* stream);
+
 /* End-to-end step from HOST buffers: H2D copies of X_host and dY_host into the
  * device staging buffers X, dY; forward(fwd) into Y; backward(bwd) into dX, dA,
  * dB; then, if `exchange` is non-NULL, exchange(exchange_user, stream) is called on

@@ -790,6 +790,21 @@ runlora_status_t forward_bf16(Ctx& c, int v, const runlora_shape_t& s, const voi
   return main_gemm(c, q, b, st);
 }
 
+// forward2's second half on a W'ᵀ [m, k] the caller built (runlora_wprime_t) — the same main
+// GEMM as forward_bf16(v = 2) issues, so the result is bit-identical.
+runlora_status_t forward_from_wpt(Ctx& c, const runlora_shape_t& s, const void* X, const void* Wpt, void* Y, Bufs& b,
+                                  cudaStream_t st) {
+  GemmReq q = main_req(c, (int)s.n, (int)s.m);
+  q.a = mat(X, s.n, s.k);
+  q.a_mn = false;
+  q.K1 = (int)s.k;
+  q.b = mat(Wpt, s.m, s.k);
+  q.b_mn = false;
+  q.D = Y;
+  q.ldd = s.m;
+  return main_gemm(c, q, b, st);
+}
+
 // backward1/5 adapter gradients: projections launch, then reductions launch whose token-split
 // slabs are summed in fixed order either by the reductions launch itself (the last split per
 // output tile, Prob::fixup) or, with `defer`, by the idle warps of the dX GEMM launch that
@@ -1369,6 +1384,38 @@ runlora_status_t runlora_backward_input(runlora_handle_t h, int bwd, const runlo
   return do_input(h, bwd, s, W, A, B, dY, dX, ws, ws_bytes, stream);
 }
 
+// ------------------------------------------------ forward2 in two halves
+runlora_status_t runlora_wprime_t(runlora_handle_t h, const runlora_shape_t* s, const void* W, const void* A,
+                                  const void* B, void* Wpt, void* stream) {
+  RL_TRY(check_handle(h));
+  RL_TRY(check_shape(s));
+  if (s->dtype != RUNLORA_BF16) return fail(RUNLORA_ERR_DTYPE, "runlora_wprime_t: bf16 operands only");
+  RL_TRY(check_ptr(W, "W"));
+  RL_TRY(check_ptr(A, "A"));
+  RL_TRY(check_ptr(B, "B"));
+  RL_TRY(check_ptr(Wpt, "Wpt"));
+  CallLock lk(h->ctx->call_mu);
+  DeviceGuard dg(h->ctx->device());
+  RL_TRY(wprime_t_bf16(*h->ctx, *s, W, A, B, Wpt, static_cast<cudaStream_t>(stream)));
+  return post_launch();
+}
+
+runlora_status_t runlora_forward_wprime(runlora_handle_t h, const runlora_shape_t* s, const void* X, const void* Wpt,
+                                        void* Y, void* ws, size_t ws_bytes, void* stream) {
+  RL_TRY(check_handle(h));
+  RL_TRY(check_shape(s));
+  if (s->dtype != RUNLORA_BF16) return fail(RUNLORA_ERR_DTYPE, "runlora_forward_wprime: bf16 operands only");
+  RL_TRY(check_ptr(X, "X"));
+  RL_TRY(check_ptr(Wpt, "Wpt"));
+  RL_TRY(check_ptr(Y, "Y"));
+  Bufs b;
+  RL_TRY(bind_ws(*s, ws, ws_bytes, &b));
+  CallLock lk(h->ctx->call_mu);
+  DeviceGuard dg(h->ctx->device());
+  RL_TRY(forward_from_wpt(*h->ctx, *s, X, Wpt, Y, b, static_cast<cudaStream_t>(stream)));
+  return post_launch();
+}
+
 // ------------------------------------------------ quantized frozen weight (R18)
 runlora_status_t runlora_quantize_w_e4m3(runlora_handle_t h, int64_t k, int64_t m, const void* W, void* Wq,
                                          float* scale, void* diag, void* stream) {
@@ -1454,6 +1501,29 @@ runlora_status_t runlora_forward_wq(runlora_handle_t h, int fwd, const runlora_s
   const QW qw{Wq, scale, diag};
   if (fwd == 1) RL_TRY(wprime_q(*h->ctx, *s, qw, nullptr, nullptr, wdq, false, false, st));
   RL_TRY(forward_bf16(*h->ctx, fwd, *s, X, wdq, A, B, Y, b, st, fwd == 2 ? &qw : nullptr));
+  return post_launch();
+}
+
+// forward2's first half from a quantized W: W'ᵀ = (W~ + A·B)ᵀ into caller memory (the same
+// fused launch runlora_forward_wq(2) issues), for runlora_forward_wprime.
+runlora_status_t runlora_wprime_t_wq(runlora_handle_t h, const runlora_shape_t* s, const void* Wq,
+                                     const float* scale, const void* diag, const void* A, const void* B, void* Wpt,
+                                     void* stream) {
+  RL_TRY(check_handle(h));
+  RL_TRY(check_shape(s));
+  if (s->dtype != RUNLORA_BF16) return fail(RUNLORA_ERR_DTYPE, "quantized W needs bf16 operands");
+  if (s->m & 15)
+    return fail(RUNLORA_ERR_ALIGNMENT, "quantized W needs m a multiple of 16 (16-byte TMA row strides of the 1-byte Wq)");
+  RL_TRY(check_ptr(Wq, "Wq"));
+  RL_TRY(check_ptr(scale, "scale"));
+  RL_TRY(check_ptr(diag, "diag"));
+  RL_TRY(check_ptr(A, "A"));
+  RL_TRY(check_ptr(B, "B"));
+  RL_TRY(check_ptr(Wpt, "Wpt"));
+  CallLock lk(h->ctx->call_mu);
+  DeviceGuard dg(h->ctx->device());
+  const QW qw{Wq, scale, diag};
+  RL_TRY(wprime_q(*h->ctx, *s, qw, A, B, Wpt, true, true, static_cast<cudaStream_t>(stream)));
   return post_launch();
 }
 

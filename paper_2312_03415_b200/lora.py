@@ -39,12 +39,46 @@ class GradSink:
             self.on_ready(self)
 
 
+class WPrimeCache:
+    """forward2's W'ᵀ = (W + A·B)ᵀ kept between calls while W, A and B are unchanged — the
+    micro-batches of one gradient-accumulation step build it once instead of once per
+    micro-batch (runlora_wprime_t, then runlora_forward_wprime per call: together forward2
+    bit for bit, include/runlora.h).  Validity is keyed on the tensors' storage and torch's
+    in-place version counters, so an optimizer step (an in-place update of A or B) or a new
+    W rebuilds it; updates through ``.data`` bypass the version counter — call
+    ``invalidate()`` after those."""
+
+    def __init__(self):
+        self.Wpt = None
+        self.key = None
+        self.builds = 0
+
+    def invalidate(self):
+        self.key = None
+
+    def get(self, h, shape, W, A, B) -> torch.Tensor:
+        w = W.q if _is_q(W) else W
+        # W' does not depend on the token count n
+        key = (w.data_ptr(), w._version, A.data_ptr(), A._version, B.data_ptr(), B._version,
+               shape.k, shape.m, shape.r)
+        if key != self.key:
+            k, m = shape.k, shape.m
+            if self.Wpt is None or tuple(self.Wpt.shape) != (m, k) or self.Wpt.device != A.device:
+                self.Wpt = torch.empty(m, k, dtype=A.dtype, device=A.device)
+            h.wprime_t(shape, W, A, B, self.Wpt)
+            self.key = key
+            self.builds += 1
+        return self.Wpt
+
+
 class LoRALinearFunction(torch.autograd.Function):
     """Y = LoRA(X) with forward variant plan.fwd and backward variant plan.bwd.
-    With a GradSink the adapter gradients go to the sink (fp32) and A.grad/B.grad stay None."""
+    With a GradSink the adapter gradients go to the sink (fp32) and A.grad/B.grad stay None.
+    With a WPrimeCache, forward2 reuses W'ᵀ while W, A and B are unchanged."""
 
     @staticmethod
-    def forward(ctx, X, W, A, B, fwd: int, bwd: int, sink: GradSink | None = None):
+    def forward(ctx, X, W, A, B, fwd: int, bwd: int, sink: GradSink | None = None,
+                wcache: WPrimeCache | None = None):
         # W: a frozen bf16/fp32 tensor, or an rl.QuantizedWeight (FP8 E4M3 + column scales)
         for t, name in ((X, "X"), (W.q if _is_q(W) else W, "W"), (A, "A"), (B, "B")):
             if not t.is_cuda or not t.is_contiguous():
@@ -52,12 +86,16 @@ class LoRALinearFunction(torch.autograd.Function):
         shape = _shape(X, W, A)
         h = rl.handle(X.device)
         Y = torch.empty(X.shape[0], W.shape[1], dtype=X.dtype, device=X.device)
-        if _is_q(W):
+        if wcache is not None and fwd == 2 and X.dtype == torch.bfloat16:
+            h.forward_wprime(shape, X, wcache.get(h, shape, W, A, B), Y)
+        elif _is_q(W):
             h.forward_wq(fwd, shape, X, W, A, B, Y)
+        else:
+            h.forward(fwd, shape, X, W, A, B, Y)
+        if _is_q(W):
             ctx.wq = W
             ctx.save_for_backward(X, A, B)  # no XA; W stays quantized
         else:
-            h.forward(fwd, shape, X, W, A, B, Y)
             ctx.wq = None
             ctx.save_for_backward(X, W, A, B)   # no XA
         ctx.bwd = bwd
@@ -81,12 +119,12 @@ class LoRALinearFunction(torch.autograd.Function):
         if sink is not None:
             run(ctx.bwd, shape, X, W, A, B, dY, dX, sink.dA, sink.dB, accumulate=sink.accumulate)
             sink.ready()
-            return dX, None, None, None, None, None, None
+            return dX, None, None, None, None, None, None, None
         gdt = torch.float32 if X.dtype == torch.float32 else A.dtype
         dA = torch.empty(A.shape, dtype=gdt, device=X.device)
         dB = torch.empty(B.shape, dtype=gdt, device=X.device)
         run(ctx.bwd, shape, X, W, A, B, dY, dX, dA, dB)
-        return dX, None, dA.to(A.dtype), dB.to(B.dtype), None, None, None
+        return dX, None, dA.to(A.dtype), dB.to(B.dtype), None, None, None, None
 
 
 def lora_linear(X, W, A, B, plan=None, criterion=rl.BY_FLOPS):

@@ -77,7 +77,7 @@ EXPORTS = ["runlora_version", "runlora_create", "runlora_destroy", "runlora_flop
            "runlora_profile_read", "runlora_launch_count", "runlora_status_string", "runlora_last_error",
            "runlora_quantize_w_e4m3", "runlora_workspace_size_wq", "runlora_forward_wq", "runlora_backward_wq",
            "runlora_allreduce_sum_f32", "runlora_exchange_sizes", "runlora_exchange_create", "runlora_exchange_destroy",
-           "runlora_backward_exchange"]
+           "runlora_backward_exchange", "runlora_wprime_t", "runlora_wprime_t_wq", "runlora_forward_wprime"]
 
 
 def _load():
@@ -115,6 +115,9 @@ def _load():
                                         C.POINTER(P)]),
         "runlora_exchange_destroy": (I, [P]),
         "runlora_backward_exchange": (I, [P, I, S, P, P, P, P, P, P, P, P, I, I, P, C.c_uint32, P, SZ, P]),
+        "runlora_wprime_t": (I, [P, S, P, P, P, P, P]),
+        "runlora_wprime_t_wq": (I, [P, S, P, P, P, P, P, P, P]),
+        "runlora_forward_wprime": (I, [P, S, P, P, P, P, SZ, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -297,6 +300,23 @@ class Handle:
                                         _DT[dA.dtype],
                                         int(bool(accumulate)), _ptr(ws), ws.numel(), _stream(self.device)),
                "runlora_backward_wq")
+
+    # ------------------------------------------------- forward2 in two halves
+    def wprime_t(self, shape, W, A, B, Wpt):
+        """runlora_wprime_t (or _wq for a QuantizedWeight): Wpt [m, k] = (W + A·B)ᵀ."""
+        if isinstance(W, QuantizedWeight):
+            _check(_lib.runlora_wprime_t_wq(self._h, C.byref(shape), _ptr(W.q), _ptr(W.scale), _ptr(W.diag),
+                                            _ptr(A), _ptr(B), _ptr(Wpt), _stream(self.device)),
+                   "runlora_wprime_t_wq")
+        else:
+            _check(_lib.runlora_wprime_t(self._h, C.byref(shape), _ptr(W), _ptr(A), _ptr(B), _ptr(Wpt),
+                                         _stream(self.device)), "runlora_wprime_t")
+
+    def forward_wprime(self, shape, X, Wpt, Y, ws=None):
+        """runlora_forward_wprime: Y = X·W' from a W'ᵀ built by wprime_t."""
+        ws = self.workspace(shape) if ws is None else ws
+        _check(_lib.runlora_forward_wprime(self._h, C.byref(shape), _ptr(X), _ptr(Wpt), _ptr(Y), _ptr(ws),
+                                           ws.numel(), _stream(self.device)), "runlora_forward_wprime")
 
     def select(self, shape: Shape, criterion=BY_FLOPS, ops: dict | None = None, grad_dtype=F32) -> Plan:
         p = Plan()

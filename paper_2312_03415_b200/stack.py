@@ -28,7 +28,7 @@ import torch.distributed as dist
 from torch import nn
 
 from . import runlora as rl
-from .lora import GradSink, LoRALinearFunction
+from .lora import GradSink, LoRALinearFunction, WPrimeCache
 
 LINEARS = ("q", "k", "v", "o", "gate", "up", "down")
 
@@ -36,9 +36,12 @@ LINEARS = ("q", "k", "v", "o", "gate", "up", "down")
 class LoRALinear(nn.Module):
     """Frozen W [k, m] (paper orientation, Y = XW) with trainable A [k, r], B [r, m].
     ``quantize_()`` replaces W by its FP8 E4M3 form with per-column scales (QLoRA-style,
-    DESIGN.md R18); forward and backward then dequantize it per call."""
+    DESIGN.md R18); forward and backward then dequantize it per call.
+    ``reuse_wprime``: with forward2, W'ᵀ = (W + AB)ᵀ is built once while W, A, B are unchanged
+    (the micro-batches of a step; lora.WPrimeCache) — one extra m x k bf16 buffer per linear;
+    off for a quantized W, whose point is the smaller resident weight."""
 
-    def __init__(self, W: torch.Tensor, A: torch.Tensor, B: torch.Tensor):
+    def __init__(self, W: torch.Tensor, A: torch.Tensor, B: torch.Tensor, reuse_wprime: bool = True):
         super().__init__()
         self.register_buffer("W", W)
         self.A = nn.Parameter(A)
@@ -47,6 +50,7 @@ class LoRALinear(nn.Module):
         self._km = tuple(W.shape)
         self.plan: Tuple[int, int] = (1, 1)
         self.sink: Optional[GradSink] = None
+        self.wcache: Optional[WPrimeCache] = WPrimeCache() if reuse_wprime else None
 
     @property
     def dims(self) -> Tuple[int, int, int]:
@@ -55,12 +59,13 @@ class LoRALinear(nn.Module):
     def quantize_(self) -> "LoRALinear":
         self.wq = rl.handle(self.W.device).quantize_w(self.W)
         self.W = None  # only the 8-bit weight and its scales stay resident
+        self.wcache = None
         return self
 
     def forward(self, x):
         fwd, bwd = self.plan
         return LoRALinearFunction.apply(x, self.wq if self.wq is not None else self.W, self.A, self.B, fwd, bwd,
-                                        self.sink)
+                                        self.sink, self.wcache)
 
 
 RMS_EPS = 1e-6

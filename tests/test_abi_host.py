@@ -111,6 +111,9 @@ def test_null_handle_is_invalid_arg(rl):
     assert lib.runlora_step_host(None, S, C.byref(st), p, 1 << 20, None) == 1
     assert lib.runlora_select(None, S, rl.BY_TIME, None, p, 1 << 20, None, C.byref(rl.Plan())) == 1
     assert lib.runlora_profile_enable(None, 1) == 1
+    assert lib.runlora_wprime_t(None, S, p, p, p, p, None) == 1
+    assert lib.runlora_wprime_t_wq(None, S, p, p, p, p, p, p, None) == 1
+    assert lib.runlora_forward_wprime(None, S, p, p, p, p, 1 << 20, None) == 1
     assert "handle" in lib.runlora_last_error().decode()
 
 
