@@ -254,12 +254,21 @@ __global__ void __launch_bounds__(256) sgemm_kernel(int M, int N, int K, const f
 }  // namespace
 
 int raster_rows(const GemmReq& r) {
-  // all of B (N x K bf16) above ~48 MB -> banded raster (see decode_unit); env RUNLORA_RASTER_G
+  // Unit order (decode_unit): G = 1 walks row tiles (every column tile of a row band of one
+  // tile), G >= the row-tile count walks column tiles, values between walk bands of G row
+  // tiles.  env RUNLORA_RASTER_G overrides.
   static const int raster_env = getenv("RUNLORA_RASTER_G") ? atoi(getenv("RUNLORA_RASTER_G")) : 0;
-  const double b_bytes = 2.0 * (double)r.N * (double)(r.K1 + r.K2);
-  // 16 measured best at C3 (8192x11008x4096: 482 µs vs 490 at 8, 492 at 1 for 512-wide
-  // tiles; 505 vs 515 for 256-wide ones)
-  return raster_env > 0 ? raster_env : b_bytes > 48e6 ? 16 : 1;
+  if (raster_env > 0) return raster_env;
+  const double K = (double)(r.K1 + r.K2);
+  const double a_bytes = 2.0 * (double)r.M * K, b_bytes = 2.0 * (double)r.N * K;
+  if (b_bytes <= 48e6) return 1;  // all of B stays in L2: row order streams A once
+  // The main GEMMs keep the SMALLER operand L2-resident and stream the other once: C3's Y
+  // GEMM 8192x11008x4096 (A 64 MB, B 90 MB) column order 476 µs vs 482 at G = 16 and 486 in
+  // row order; its dX GEMM 8192x4096x11008 (A 180 MB, B 90 MB) row order 449.5 µs vs 455.7
+  // at G = 16 (tools/gemm_bench.py, RUNLORA_RASTER_G sweep, profiles/r02/raster_sweep.txt)
+  if (r.kid == KID_GEMM_MAIN && a_bytes < b_bytes && a_bytes <= 100e6) return std::max(1, (r.M + 127) / 128);
+  if (r.kid == KID_GEMM_MAIN && b_bytes <= 100e6) return 1;
+  return 16;  // neither fits: bands of 16 row tiles
 }
 
 cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t s, std::string* err) {
