@@ -42,8 +42,11 @@ def test_planner_split(rl):
     # MN-major B (forward1's Y GEMM) and single-round shapes stay 256-wide
     assert _rows(rl, h, 8192, 4096, 4096, b_mn=1) == 0
     assert _rows(rl, h, 512, 512, 512) == 0
-    # short K: the exposed epilogue outweighs the traffic saving
-    assert _rows(rl, h, 4096, 3000, 776) == 0
+    # short K: with the tile held in registers the wide tiles pay even at 13 k-blocks; the
+    # planner mixes them with 256-wide rows (measured 31.7 µs mixed vs 33.8 either pure,
+    # DESIGN.md §5)
+    r = _rows(rl, h, 4096, 3000, 776)
+    assert 0 < r < 4096 and r % 256 == 0
 
 
 CASES = [synth.case("wide_w1", 0, 40, 3000, 2048, 3304, 16, "bf16"),
