@@ -23,8 +23,13 @@
 //   warp 2        : TMEM allocator (2 accumulator slots of min(BN_MAX, 256) columns: the
 //                   epilogue of tile i overlaps the mainloop of tile i+1; BN_MAX = 512 pair
 //                   tiles issue two N = 256 MMAs per k-step sharing the A tile and use both)
+//   warps 2-3     : side jobs while the mainloop runs (slab reduction, column repeat, the
+//                   fused DP exchange), else idle
 //   warps 4..7    : epilogue (tcgen05.ld -> registers -> global, or -> swizzled smem ->
-//                   TMA store for EPI = 3), TMEM lanes 32*(w%4)..
+//                   TMA store for EPI = 3), TMEM lanes 32*(w%4)..; the 512-wide TMA-store
+//                   kernel runs warps 4..11 (two per lane quarter, 128 columns each) with a
+//                   setmaxnreg split, holding the whole tile in registers so TMEM is released
+//                   before the stores (TileCfg::WIDE_HOLD)
 // Tiles: 128 rows per CTA, bn columns (runtime, <= BN_MAX), K atoms of 64 (one 128-byte
 // swizzle row of bf16), KS atoms per pipeline stage.  Shared-memory tiles use the 128B
 // swizzle written by TMA:
