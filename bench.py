@@ -40,7 +40,9 @@ METRIC = "LoRA-linear fwd+bwd tokens/s, tensor-pipe util, speedup vs default XW+
 UNIT = "tokens/s"
 CAPTION = "synthetic: seeded i.i.d. Gaussian operands with BASELINE.json's laws (no dataset/weights)"
 ORACLE_SLICE = 1024  # tokens per oracle slice (cpu_baseline and the reference arm alike)
-E2E_SETS = 3  # steps in flight in the e2e leg (own streams, device buffers and workspaces)
+# steps in flight in the e2e leg (own streams, device buffers and workspaces): 4 measured best
+# (2.77-2.79 M tokens/s vs 2.70 with 3 and 2.59 with 6 at C2)
+E2E_SETS = int(os.environ.get("RUNLORA_E2E_SETS", "4"))
 
 
 def _peaks():
@@ -436,11 +438,11 @@ def main():
     # ---------------- end to end through the C ABI with host buffers
     # Every step: H2D of its X, dY from pinned host memory, forward + backward (+ the DP
     # allreduce through the exchange hook at N > 1), D2H of dA, dB and of Y, dX
-    # (runlora_step_host).  Three steps are in flight on three streams with their own device
-    # buffers and workspaces: a stream runs its step's H2D, kernels and D2H in order, so with
-    # three of them one step's inputs stream in while another's outputs stream out and a third
-    # computes — both PCIe directions stay busy (tools/pcie_probe.py: 128 MiB each way take
-    # 2.7 ms concurrently, the floor of a C2 step's 256 MiB of copies).
+    # (runlora_step_host).  E2E_SETS steps are in flight on as many streams with their own
+    # device buffers and workspaces: a stream runs its step's H2D, kernels and D2H in order, so
+    # with several of them one step's inputs stream in while another's outputs stream out and
+    # a third computes — both PCIe directions stay busy (tools/pcie_probe.py: 128 MiB each way
+    # take 2.7 ms concurrently, the floor of a C2 step's 256 MiB of copies).
     hx = ops["X"].pin_memory()
     hdy = ops["dY"].pin_memory()
     sets = []
