@@ -244,6 +244,7 @@ def main():
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--c5-steps", type=int, default=2)
+    ap.add_argument("--no-wprime-reuse", action="store_true", help="C5: rebuild W' every micro-batch")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the multi-rank code path on one GPU (not a performance mode)")
     args = ap.parse_args()
@@ -671,6 +672,8 @@ def c5_stack(args, rl, dist, dev, local, world, rank, timed):
     per_rank = n_glob // world
     micro = max(1, per_rank // mb)
     model = build(layers, d, f, r, dev)
+    if not args.no_wprime_reuse:
+        model.reuse_wprime_(True)  # W'ᵀ once per step, reused by the micro-batches (R20)
     plans = plan_model(model, mb, rl.BY_TIME)
     if world > 1:  # every rank runs rank 0's plans
         t = torch.tensor([v for _, _, lin in model.linears() for v in lin.plan], device=dev)
@@ -690,18 +693,35 @@ def c5_stack(args, rl, dist, dev, local, world, rank, timed):
             model(xi).backward(dy)
         sync.finish()
 
+    def peak_extra(fn):
+        """Peak device memory of one step above what is resident before it (activations,
+        saved tensors, workspaces) — the quantity the paper's memory claim is about."""
+        torch.cuda.synchronize(dev)
+        before = torch.cuda.memory_allocated(dev)
+        torch.cuda.reset_peak_memory_stats(dev)
+        fn()
+        torch.cuda.synchronize(dev)
+        return torch.cuda.max_memory_allocated(dev) - before
+
     w = max(1, min(args.warmup, 1))
     for _ in range(w):
         step()
     ms = timed(step, args.c5_steps)
+    mem = peak_extra(step)
+    cache_bytes = sum(lin.wcache.Wpt.numel() * 2 for _, _, lin in model.linears()
+                      if lin.wcache is not None and lin.wcache.Wpt is not None)
     out = {"workload": "C5_stack_32L", "layers": layers, "r": r, "global_tokens": n_glob,
            "tokens_per_rank": per_rank, "micro_batches": micro, "micro_batch_tokens": mb,
            "plans": {f"{k}x{m}": f"F{int(p.fwd)}+B{int(p.bwd)}" for (k, m, _), p in plans.items()},
            "steps": args.c5_steps, "warmup": w, "ms_per_step": ms, "tokens_per_s": n_glob / (ms * 1e-3),
            "parallelism": f"dp{world} token-sharded, bucketed NCCL allreduce of fp32 adapter grads",
            "wprime_reuse": all(lin.wcache is not None for _, _, lin in model.linears()),
-           "note": "forward2's W'ᵀ built once per step per linear and reused by the micro-batches "
-                   "(runlora_wprime_t + runlora_forward_wprime, lora.WPrimeCache)"}
+           "wprime_cache_bytes": cache_bytes,
+           "step_peak_extra_bytes": mem,
+           "note": "wprime_reuse: forward2's W'ᵀ built once per step per linear and reused by the "
+                   "micro-batches (runlora_wprime_t + runlora_forward_wprime, lora.WPrimeCache; "
+                   "resident, wprime_cache_bytes); step_peak_extra_bytes: peak memory of one step above "
+                   "the resident weights and caches"}
     if not args.no_default_chain:
         base = LoRAStack([LoRALayer({nm: DefaultLinear(L.lin[nm]) for nm in LINEARS}) for L in model.layers]).to(dev)
         if world > 1:
@@ -721,6 +741,7 @@ def c5_stack(args, rl, dist, dev, local, world, rank, timed):
         for _ in range(w):
             default_step()
         ms_def = timed(default_step, args.c5_steps)
+        out["default_step_peak_extra_bytes"] = peak_extra(default_step)
         out["default_ms_per_step"] = ms_def
         out["speedup_vs_default"] = ms_def / ms
         del base

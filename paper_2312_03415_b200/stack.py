@@ -38,10 +38,11 @@ class LoRALinear(nn.Module):
     ``quantize_()`` replaces W by its FP8 E4M3 form with per-column scales (QLoRA-style,
     DESIGN.md R18); forward and backward then dequantize it per call.
     ``reuse_wprime``: with forward2, W'ᵀ = (W + AB)ᵀ is built once while W, A, B are unchanged
-    (the micro-batches of a step; lora.WPrimeCache) — one extra m x k bf16 buffer per linear;
-    off for a quantized W, whose point is the smaller resident weight."""
+    (the micro-batches of a step; lora.WPrimeCache) — one extra m x k bf16 buffer per linear,
+    so off by default (nothing but W, A, B persists between calls, R20) and off for
+    a quantized W, whose point is the smaller resident weight."""
 
-    def __init__(self, W: torch.Tensor, A: torch.Tensor, B: torch.Tensor, reuse_wprime: bool = True):
+    def __init__(self, W: torch.Tensor, A: torch.Tensor, B: torch.Tensor, reuse_wprime: bool = False):
         super().__init__()
         self.register_buffer("W", W)
         self.A = nn.Parameter(A)
@@ -108,6 +109,13 @@ class LoRAStack(nn.Module):
     def linears(self) -> List[Tuple[int, str, LoRALinear]]:
         """(layer, name, module) in forward order."""
         return [(i, nm, L.lin[nm]) for i, L in enumerate(self.layers) for nm in LINEARS]
+
+    def reuse_wprime_(self, enable: bool = True) -> "LoRAStack":
+        """forward2's W'ᵀ built once per optimizer step per linear and reused by the step's
+        micro-batches (one extra m x k bf16 buffer per linear; no effect on quantized linears)."""
+        for _, _, lin in self.linears():
+            lin.wcache = WPrimeCache() if enable and lin.wq is None else None
+        return self
 
     def quantize_(self) -> "LoRAStack":
         """Every frozen W to FP8 E4M3 + per-column scales (QLoRA-style fine-tuning)."""

@@ -77,8 +77,9 @@ def test_wprime_cache_micro_batches_and_updates(rl):
     from paper_2312_03415_b200.stack import LoRALinear
     c = synth.case("wp_cache", 0, 92, 768, 512, 1024, 16, "bf16")
     ops = synth.operands(c)
-    lin = LoRALinear(ops["W"].cuda(), ops["A"].cuda(), ops["B"].cuda())
-    plain = LoRALinear(ops["W"].cuda(), ops["A"].cuda(), ops["B"].cuda(), reuse_wprime=False)
+    lin = LoRALinear(ops["W"].cuda(), ops["A"].cuda(), ops["B"].cuda(), reuse_wprime=True)
+    plain = LoRALinear(ops["W"].cuda(), ops["A"].cuda(), ops["B"].cuda())
+    assert plain.wcache is None  # off by default: nothing but W, A, B persists (R20)
     lin.plan = plain.plan = (2, 1)
     X = ops["X"].cuda()
     chunks = [X[i:i + 256] for i in range(0, c.n, 256)]

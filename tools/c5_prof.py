@@ -28,9 +28,7 @@ def main():
     d, f, r, mb = 4096, 11008, 16, 8192
     model = build(a.layers, d, f, r, dev)
     plan_model(model, mb, rl.BY_TIME)
-    if a.no_reuse:
-        for _, _, lin in model.linears():
-            lin.wcache = None
+    model.reuse_wprime_(not a.no_reuse)
     sync = BucketedGradSync.for_model(model)
     g = torch.Generator(device=dev).manual_seed(7)
     xs = [torch.randn(mb, d, generator=g, device=dev).to(torch.bfloat16) for _ in range(a.micro)]
