@@ -101,3 +101,21 @@ def test_guards_fused_exchange(rl):
             assert g[k].intact(), k
     finally:
         rl.exchange_destroy(x)
+
+
+@pytest.mark.parametrize("c", CASES[:2], ids=lambda c: c.name)
+def test_guards_forward2_halves(rl, c):
+    """runlora_wprime_t / _wq write exactly the m x k W'ᵀ; runlora_forward_wprime exactly Y."""
+    d = {k: v.cuda() for k, v in synth.operands(c).items()}
+    h = rl.handle(0)
+    shape = rl.make_shape(c.n, c.k, c.m, c.r, rl.BF16)
+    wg = Guarded(c.m * c.k * 2)
+    Wpt = wg.view((c.m, c.k), torch.bfloat16)
+    g, t = _outputs(c)
+    h.wprime_t(shape, d["W"], d["A"], d["B"], Wpt)
+    h.forward_wprime(shape, d["X"], Wpt, t["Y"])
+    if c.m % 16 == 0:
+        h.wprime_t(shape, h.quantize_w(d["W"]), d["A"], d["B"], Wpt)
+        h.forward_wprime(shape, d["X"], Wpt, t["Y"])
+    torch.cuda.synchronize()
+    assert wg.intact() and g["Y"].intact()
