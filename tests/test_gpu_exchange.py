@@ -44,6 +44,28 @@ def _emulate(rl, h, P, k, m, r, splits, sA, sB, epoch, bufs, flags):
     return dA, dB
 
 
+def test_emulated_exchange_long_run(rl):
+    """200 consecutive epochs of the 8-rank emulated exchange on the same buffers (alternating
+    halves, reused flags): every epoch bit-identical to the first — a flag or buffer-half race
+    would show up as a changed bit or a hang (bounded by the pytest timeout)."""
+    P, k, m, r, splits = 8, 520, 392, 16, 3
+    h = rl.handle(0)
+    buf_bytes, flag_bytes = rl.exchange_sizes(k, m, r, P)
+    bufs = [torch.zeros(buf_bytes // 4, device="cuda") for _ in range(P)]
+    flags = [torch.zeros(flag_bytes // 4, dtype=torch.int32, device="cuda") for _ in range(P)]
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7)
+    sA = [torch.randn(splits, k, r, device="cuda", generator=g) for _ in range(P)]
+    sB = [torch.randn(splits, m, r, device="cuda", generator=g) for _ in range(P)]
+    ref = None
+    for epoch in range(1, 201):
+        dA, dB = _emulate(rl, h, P, k, m, r, splits, sA, sB, epoch, bufs, flags)
+        if ref is None:
+            ref = (dA[0].clone(), dB[0].clone())
+        for q in range(P):
+            assert torch.equal(dA[q], ref[0]) and torch.equal(dB[q], ref[1]), (epoch, q)
+
+
 @pytest.mark.parametrize("P", [1, 2, 4, 8])
 def test_emulated_exchange_bit_exact(rl, P):
     k, m, r, splits = 520, 392, 16, 3

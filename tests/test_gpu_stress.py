@@ -53,3 +53,30 @@ def test_back_to_back_steps_bit_identical(rl, plan):
     wA, wB = O.adapter_grads(ops["X"].float().numpy(), A, B, ops["dY"].float().numpy())
     assert O.rel_fro(ref["dA"].double().cpu().numpy(), wA) < 5e-3
     assert O.rel_fro(ref["dB"].double().cpu().numpy(), wB) < 5e-3
+
+
+def test_quantized_w_back_to_back_bit_identical(rl):
+    """The quantized-W path (FP8 tail GEMMs building W' / W'ᵀ from Wq, R18) under
+    the same long-run determinism check, F2+B5 (its time pick) and F2+B1 (W~ materialised)."""
+    c = synth.C2[16]
+    d = {k: v.cuda() for k, v in synth.operands(c).items()}
+    h = rl.handle(0)
+    shape = rl.make_shape(c.n, c.k, c.m, c.r, rl.BF16)
+    qw = h.quantize_w(d["W"])
+    ws = h.workspace(shape, quantized_w=True)
+    out = {"Y": torch.empty(c.n, c.m, dtype=torch.bfloat16, device="cuda"),
+           "dX": torch.empty(c.n, c.k, dtype=torch.bfloat16, device="cuda"),
+           "dA": torch.empty(c.k, c.r, device="cuda"), "dB": torch.empty(c.r, c.m, device="cuda")}
+    for fwd, bwd in ((2, 5), (2, 1)):
+        def step():
+            h.forward_wq(fwd, shape, d["X"], qw, d["A"], d["B"], out["Y"], ws=ws)
+            h.backward_wq(bwd, shape, d["X"], qw, d["A"], d["B"], d["dY"], out["dX"], out["dA"], out["dB"], ws=ws)
+
+        step()
+        ref = {k: v.clone() for k, v in out.items()}
+        bad = torch.zeros((), dtype=torch.int64, device="cuda")
+        for _ in range(STEPS // 2):
+            step()
+            bad += torch.stack([(out[k] != ref[k]).any() for k in ("Y", "dX", "dA", "dB")]).any().long()
+        torch.cuda.synchronize()
+        assert int(bad) == 0, (fwd, bwd, int(bad))
