@@ -361,8 +361,9 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
     p.fold = r.fold;
     p.fold_w = r.fold_w;
     if (r.out_mode == OUT_F32_FOLD &&
-        (!(r.fold_w == 8 || r.fold_w == 16 || r.fold_w == 32) || r.fold * r.fold_w != r.BN || r.BN > 256)) {
-      if (err) *err = "tc_gemm: OUT_F32_FOLD needs fold_w in {8, 16, 32} and BN = fold * fold_w";
+        (!(r.fold_w == 8 || r.fold_w == 16 || r.fold_w == 32 || r.fold_w == 64) || r.fold * r.fold_w != r.BN ||
+         r.BN > 256 || cg != 1)) {
+      if (err) *err = "tc_gemm: OUT_F32_FOLD needs single-CTA tiles, fold_w in {8, 16, 32, 64} and BN = fold * fold_w";
       return cudaErrorInvalidValue;
     }
     p.tail_diag = r.tail_diag ? 1 : 0;

@@ -331,14 +331,17 @@ ZPlan plan_z(const runlora_shape_t& s) {
   f.bn_z[1] = skinny_bn(r, true);   // Z2: B_op = A [k, r] (MN-major)
   if (r > f.bn_z[0] || r > f.bn_z[1]) return f;  // one n tile per projection
   // sz: split K only while the projections' 2*mt row tiles leave SMs idle (2*mt*sz <= one
-  // wave of 2 CTAs/SM), within sz*r in {16, 32, 64} (a legal MN-major tile width that keeps
-  // the reductions on the 2-CTA/SM kernel) and r a fold width (8, 16, 32).  At C2 (mt = 64,
-  // r = 16) this gives sz = 2: projections 41 -> 34 µs, plus a 1.5 µs A repeat for backward1.
+  // wave of 2 CTAs/SM), within sz*r in {16, 32, 64} — 128 for r = 64 — (a legal MN-major tile
+  // width that keeps the reductions on the 2-CTA/SM kernel) and r a fold width (8, 16, 32,
+  // 64).  At C2 (mt = 64) this gives sz = 2 for r = 16 (projections 41 -> 34 µs) and for
+  // r = 64 (40 -> 27 µs; the reductions +2 µs and backward1's dX tail one more k-block:
+  // steps 0.958-0.967x, profiles/r02/ab_z64.jsonl).  env RUNLORA_ZSPLIT64=0: sz = 1 at r = 64.
   const int64_t kbz[2] = {(m + kBK - 1) / kBK, (k + kBK - 1) / kBK};
   int sz = 1;
-  if ((r == 8 || r == 16 || r == 32) && 2 * mt < 148) {
+  static const bool split64 = getenv("RUNLORA_ZSPLIT64") == nullptr || atoi(getenv("RUNLORA_ZSPLIT64")) != 0;
+  if ((r == 8 || r == 16 || r == 32 || (r == 64 && split64)) && 2 * mt < 148) {
     for (int c = 2; c <= 8 && 2 * mt * c <= 2 * 148; c *= 2) {
-      if (c * r > 64) break;
+      if (c * r > (r == 64 ? 128 : 64)) break;
       bool even = true;
       for (int i = 0; i < 2; ++i) {
         const int64_t kp = (kbz[i] + c - 1) / c;

@@ -869,11 +869,11 @@ __global__ void __launch_bounds__(TileCfg<BN_MAX, CG, OCC, EPI, KS>::THREADS, OC
             reg_fence32(v[1]);
             stage_store_chunk<C::STG_BUFS>(v, stg, st_it, lane, dmap, nc + 64 * i, m0 + q * 32);
           }
-        } else if (p.out_mode == OUT_F32_FOLD) {
-          // sum of the fold column blocks (w = fold_w in {8, 16, 32}), in block order
-          float o[32];
+        } else if (CG == 1 && p.out_mode == OUT_F32_FOLD) {  // token reductions only (single-CTA kernels)
+          // sum of the fold column blocks (w = fold_w in {8, 16, 32, 64}), in block order
+          float o[64];
 #pragma unroll
-          for (int x = 0; x < 32; ++x) o[x] = 0.f;
+          for (int x = 0; x < 64; ++x) o[x] = 0.f;
           const int w = p.fold_w;
 #pragma unroll 1
           for (int c = 0; c < bw; c += 32) {
@@ -882,7 +882,15 @@ __global__ void __launch_bounds__(TileCfg<BN_MAX, CG, OCC, EPI, KS>::THREADS, OC
             if (full32) tmem_ld_32x32b_x32(t_row + c, v);
             else tmem_ld_32x32b_x16(t_row + c, v);
             tmem_ld_wait();
-            if (w == 32) {
+            if (w == 64) {  // 32-column chunk c/32 is half (c/32) & 1 of its 64-wide block
+              if ((c & 32) == 0) {
+#pragma unroll
+                for (int x = 0; x < 32; ++x) o[x] += __uint_as_float(v[x]);
+              } else {
+#pragma unroll
+                for (int x = 0; x < 32; ++x) o[32 + x] += __uint_as_float(v[x]);
+              }
+            } else if (w == 32) {
 #pragma unroll
               for (int x = 0; x < 32; ++x) o[x] += __uint_as_float(v[x]);
             } else if (w == 16) {
@@ -904,7 +912,7 @@ __global__ void __launch_bounds__(TileCfg<BN_MAX, CG, OCC, EPI, KS>::THREADS, OC
           if (row < p.M) {
             float* dst = static_cast<float*>(p.D) + t.split * p.split_stride + (long long)row * p.ldd;
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
+            for (int e = 0; e < 16; ++e)
               if (4 * e < w) *reinterpret_cast<float4*>(dst + 4 * e) = make_float4(o[4 * e], o[4 * e + 1], o[4 * e + 2], o[4 * e + 3]);
           }
         } else if (bw % 32 == 0) {
