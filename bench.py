@@ -539,6 +539,10 @@ def main():
             hbm_roof[nm]["work_us_per_launch"] = work[nm]
             hbm_roof[nm]["achieved_work"] = per_launch / (work[nm] * 1e-6) / 1e9
             hbm_roof[nm]["frac_work"] = hbm_roof[nm]["achieved_work"] / hbm
+        hbm_roof[nm]["note"] = ("achieved/frac: CUDA events around each launch in the profile pass — the events "
+                                "break the PDL chain, so each interval also holds a launch latency (~4 us); "
+                                "achieved_work/frac_work: the launch's own span from the kernel's timestamps "
+                                "(first CTA past the PDL wait -> last CTA exit) in the timed steps")
     roof["hbm_kernels"] = hbm_roof
 
     if rank == 0:
