@@ -540,7 +540,8 @@ def main():
             hbm_roof[nm]["achieved_work"] = per_launch / (work[nm] * 1e-6) / 1e9
             hbm_roof[nm]["frac_work"] = hbm_roof[nm]["achieved_work"] / hbm
         hbm_roof[nm]["note"] = ("achieved/frac: CUDA events around each launch in the profile pass — the events "
-                                "break the PDL chain, so each interval also holds a launch latency (~4 us); "
+                                "break the PDL chain, so each interval also holds the launch latency and the CTAs' "
+                                "start-up that PDL otherwise overlaps with the previous kernel; "
                                 "achieved_work/frac_work: the launch's own span from the kernel's timestamps "
                                 "(first CTA past the PDL wait -> last CTA exit) in the timed steps")
     roof["hbm_kernels"] = hbm_roof
