@@ -418,6 +418,14 @@ cudaError_t launch_tc_gemm(Ctx& ctx, const GemmReq* reqs, int nreq, cudaStream_t
   // drop from 4 to 3 (frees 48 KB) instead of being clamped to the full ring
   if (g.stages > 0 && g.stages < 7 && bn_max > 256) g.stages = 3;
   if (const char* d = getenv("RUNLORA_DBG_GEMM")) g.dbg = atoi(d);
+  {
+    // 512-wide tiles: the last 3 k-blocks issue MMA 0 before MMA 1 so slot s0 drains under
+    // MMA 1's tail (MMA-only run at 131072x2048x2048 554 -> 534 µs; steps 0.991-0.995x,
+    // profiles/r02/ab_endj.jsonl); env RUNLORA_ENDJ=0 turns it off
+    static const int endj = getenv("RUNLORA_ENDJ") ? atoi(getenv("RUNLORA_ENDJ")) : 3;
+    const int st = g.stages > 0 ? g.stages : 4;
+    g.endj = std::max(0, std::min(endj, st - 1));
+  }
   for (int q = nreq; q < kMaxProb; ++q) g.p[q] = g.p[0], g.px[q] = g.px[0], g.p[q].units = 0;
   if (g.total_units <= 0) return cudaSuccess;
   // a CTA defers at most kMaxFixups split fix-ups to the end of its unit loop; beyond that

@@ -133,6 +133,7 @@ struct GemmArgs {
   unsigned long long* trace;
   unsigned long long* ltrace;  // launch timeline slot (nullptr: off)
   int stages;                  // pipeline stages (0: the compiled maximum TileCfg::STAGES)
+  int endj;                    // 512-wide tiles: k-blocks whose MMA 1 follows the tile's last MMA 0
   int* zero_ptr;               // zeroed by CTA 0 after the PDL wait (split fix-up counters of a
   int zero_n;                  // later launch in the stream), nullptr: none
   SideJob side[2];
@@ -733,7 +734,11 @@ __global__ void __launch_bounds__(TileCfg<BN_MAX, CG, OCC, EPI, KS>::THREADS, OC
         }
         i_start = npre * KS;
       }
-      for (int i0 = i_start; i0 < nkb; i0 += KS) {
+      // 512-wide tile: its last `endj` k-blocks run MMA 0 first and hand slot s0 to the
+      // epilogue, then MMA 1 on the same (held) ring slots — the epilogue reads slot s0 while
+      // the tensor core finishes slot s0 ^ 1
+      const int endj = (BN_MAX > SLOT_W && nh == 2 && KS == 1 && nkb - i_start > g.endj) ? g.endj : 0;
+      for (int i0 = i_start; i0 < nkb - endj; i0 += KS) {
         if (g.dbg != 1 && g.dbg != 3 && g.dbg != 4) mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (elect_one_sync()) {
@@ -746,11 +751,37 @@ __global__ void __launch_bounds__(TileCfg<BN_MAX, CG, OCC, EPI, KS>::THREADS, OC
           phase ^= 1;
         }
       }
-      if (elect_one_sync()) {  // accumulator(s) ready for the epilogue(s)
-        umma_commit<CG>(&tfull[s0]);
-        if (nh == 2) umma_commit<CG>(&tfull[s0 ^ 1]);
+      if (BN_MAX > SLOT_W && endj > 0) {
+        const int st0 = stage;
+        for (int j = 0; j < endj; ++j) {
+          if (g.dbg != 1 && g.dbg != 3 && g.dbg != 4) mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one_sync()) issue(stage, nkb - endj + j, 1);
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (elect_one_sync()) umma_commit<CG>(&tfull[s0]);
+        __syncwarp();
+        for (int j = 0; j < endj; ++j) {
+          const int st = (st0 + j) % STAGES;
+          if (elect_one_sync()) {
+            issue(st, nkb - endj + j, 2);
+            umma_commit<CG>(&empty[st]);
+          }
+          __syncwarp();
+        }
+        if (elect_one_sync()) umma_commit<CG>(&tfull[s0 ^ 1]);
+        __syncwarp();
+      } else {
+        if (elect_one_sync()) {  // accumulator(s) ready for the epilogue(s)
+          umma_commit<CG>(&tfull[s0]);
+          if (nh == 2) umma_commit<CG>(&tfull[s0 ^ 1]);
+        }
+        __syncwarp();
       }
-      __syncwarp();
       for (int h = 0; h < nh; ++h) {
         if (s0 ^ h) ++use1;
         else ++use0;
